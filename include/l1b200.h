@@ -1,0 +1,110 @@
+/*
+ * l1b200.h -- C ABI of the B200-native sparse l1 line-fit hot path.
+ *
+ * The reference (l1line, /root/reference/pkg/src/l1line) is pure Python on
+ * NumPy and has no FFI of its own; each entry point below replaces the
+ * Python function named beside it, with the same argument meaning.  The
+ * Python mirror of the reference API (paper_2402_16712_b200/api.py) binds
+ * these through ctypes; INTEGRATION.md shows the binding a maintainer would
+ * add to l1line itself.
+ *
+ * Conventions
+ *   - Every pointer named d_* is DEVICE memory; h_* is host memory.
+ *   - X is the data matrix exactly as DataMatrix.values holds it
+ *     (core.py:45-68): row-major, n rows x m columns, float64, ld = m.
+ *   - All work is enqueued on `stream` (a cudaStream_t passed as void*);
+ *     no call synchronises unless its comment says so.  The library owns no
+ *     device memory: callers pass a workspace of l1b_workspace_bytes().
+ *   - Status codes: 0 = OK, negative = error (see l1b_status_string).  No C++
+ *     exception ever crosses this boundary.
+ */
+#ifndef L1B200_H
+#define L1B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define L1B_OK 0
+#define L1B_EINVAL -1   /* bad shape / index / lambda -> ValueError or IndexError */
+#define L1B_ECUDA -2    /* CUDA launch or runtime failure                          */
+#define L1B_ENOMEM -3   /* workspace too small                                     */
+#define L1B_EINTERNAL -4
+
+/* Human-readable text for a status code. */
+const char* l1b_status_string(int status);
+
+/* ABI version (bumped on any signature change). */
+int l1b_version(void);
+
+/* Bytes of device workspace needed by l1b_prepare + l1b_fit_pivots for an
+ * n x m matrix, nlam penalty weights and npiv pivots in the shard. */
+size_t l1b_workspace_bytes(int64_t n, int64_t m, int32_t nlam, int64_t npiv);
+
+/* K0: per-column statistics and the pivot-major tableau records.
+ * Replaces the lambda-independent half of ratios.py:109-135 (pivot_tableau:
+ * nonzero rows, weights |x_ip|) for every pivot at once, plus the column
+ * sums sum_i |x_ij| that core.py:93 (residual_error) needs for dead columns
+ * and degenerate pivots (fit.py:66-72).  Must run before l1b_fit_pivots on
+ * the same workspace whenever X changes. */
+int l1b_prepare(const double* d_X, int64_t n, int64_t m, void* d_ws, size_t ws_bytes,
+                void* stream);
+
+/* K1 + K2: Algorithm 1 for the pivots {p_begin + k*p_stride : 0 <= k < npiv}
+ * and nlam penalty weights h_lams[0..nlam).
+ * Replaces fit.py:75-85 (fit_for_pivot) for each pivot and the per-pivot
+ * half of fit.py:88-102 (fit_line) -- everything except the final argmin,
+ * which l1b_argmin performs.  Outputs (device, lambda-major):
+ *   d_V   [nlam][npiv][m]  direction per pivot (v[p] = 1, or all 0 for a
+ *                          zero pivot column); may be NULL if not wanted
+ *   d_err [nlam][npiv]     sum_ij |x_ij - v_j x_ip|       (core.py:93)
+ *   d_pen [nlam][npiv]     sum_j |v_j|                    (core.py:131)
+ *   d_obj [nlam][npiv]     err + lam * pen                (core.py:133)
+ * Rejects lambda < 0 or NaN (fit.py:20-24); +inf is accepted. */
+int l1b_fit_pivots(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam,
+                   int64_t p_begin, int64_t p_stride, int64_t npiv, double* d_V, double* d_err,
+                   double* d_pen, double* d_obj, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Reduction half of fit.py:98-102: per lambda, the strict '<' argmin of
+ * d_obj[l][0..npiv) in ascending pivot order (ties -> smallest pivot).
+ * Writes d_best_k[l] (index into the shard) and d_best_obj[l]. */
+int l1b_argmin(const double* d_obj, int32_t nlam, int64_t npiv, int64_t* d_best_k,
+               double* d_best_obj, void* stream);
+
+/* core.py:79-93 with NumPy's exact pairwise summation order over the
+ * row-major flattened n*m residual |x_ij - fl(x_ip * v_j)|, so the returned
+ * error is bit-identical to residual_error() in the reference.  Used to
+ * re-score the winning pivot(s).  d_out is one double. */
+int l1b_residual_exact(const double* d_X, int64_t n, int64_t m, const double* d_v, int64_t p,
+                       double* d_out, void* d_ws, size_t ws_bytes, void* stream);
+
+/* subspace.py:22-36 deflate: X <- X - (X w) w^T with w = v / ||v||_2, in
+ * place.  d_tmp must hold n + 1 doubles. */
+int l1b_deflate(double* d_X, int64_t n, int64_t m, const double* d_v, double* d_tmp, void* stream);
+
+/* max_ij |x_ij| into d_out[0] (the early-stop test of subspace.py:67,71). */
+int l1b_absmax(const double* d_X, int64_t n, int64_t m, double* d_out, void* stream);
+
+/* Self-test of the bit-exact division used by K1 (no reference counterpart;
+ * it backs the parity claim for ratios.py:119 R = X[rows,t] / x_p): n_pairs
+ * random (a, b) in the SAFE exponent window, counting results that differ
+ * from IEEE __ddiv_rn into *d_mismatches (device uint64). */
+int l1b_selftest_divide(uint64_t seed, int64_t n_pairs, uint64_t* d_mismatches, void* stream);
+
+/* Cumulative count of kernels this library has enqueued in the process
+ * (benchmark evidence for "gpu_launches"; no reference counterpart). */
+uint64_t l1b_kernel_launches(void);
+
+/* FP64 pipe probe: `blocks` x `threads` threads each run 8 independent DFMA
+ * chains of `iters` steps (8 * iters FMAs per thread).  bench.py times it
+ * with CUDA events to measure the FP64 peak the roofline is quoted against.
+ * d_out: one device double (written only to keep the chains alive). */
+int l1b_dfma_probe(int64_t iters, int32_t blocks, int32_t threads, double* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L1B200_H */

@@ -1,0 +1,31 @@
+"""B200-native sparse l1 best-fit lines (arXiv 2402.16712, Algorithm 1).
+
+A drop-in for the hot path of the reference package ``l1line``: the same
+``fit_line`` / ``fit_for_pivot`` / ``fit_subspace`` API and ``FittedLine``
+results, computed by hand-written sm_100a CUDA kernels behind a C ABI
+(``include/l1b200.h``).  Importing the package is cheap and works without a
+GPU (types, data generation); the first fit loads ``csrc/libl1b200.so`` and
+requires a CUDA device -- there is no CPU fallback.
+"""
+
+from .core import DataMatrix, EmptyPivotError, FittedLine, SubspaceFit
+from .datagen import gen_line_data, gen_outlier_data, laplace
+
+__version__ = "0.1.0"
+
+_API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
+        "residual_error", "resolve_threads")
+
+__all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "SubspaceFit", "gen_line_data",
+           "gen_outlier_data", "laplace", "use_gpu", *_API, "__version__"]
+
+
+def __getattr__(name):
+    # The device API pulls in torch; load it on first use only.
+    if name in _API:
+        from . import api
+        return getattr(api, name)
+    if name == "use_gpu":
+        from .integration import use_gpu
+        return use_gpu
+    raise AttributeError(name)

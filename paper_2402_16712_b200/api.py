@@ -1,0 +1,158 @@
+"""Drop-in mirror of the reference's fit API, running on the B200.
+
+Same names, arguments, results and error behaviour as ``l1line``
+(``/root/reference/pkg/src/l1line``) for the hot path:
+
+* ``fit_line(data, lam, threads=None)``        <- fit.py:88-102
+* ``fit_for_pivot(data, pivot, lam)``          <- fit.py:75-85
+* ``degenerate_line(data, pivot, lam)``        <- fit.py:66-72
+* ``fit_subspace(data, lam, k, threads=None)`` <- subspace.py:54-76
+* ``deflate(data, v)``                         <- subspace.py:22-36
+* ``residual_error(data, v, preserved)``       <- core.py:79-93
+
+plus ``fit_lines(data, lams)``, the batched lambda sweep the reference can
+only do as repeated ``fit_line`` calls (BASELINE config C3).
+
+``threads`` is validated like ``resolve_threads`` (parallel.py:19-33) and
+otherwise ignored: the GPU grid replaces the thread pool.  Inputs may be a
+``DataMatrix`` from this package, a reference ``l1line.DataMatrix`` (duck
+typed on ``.values``) or an array-like.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+
+from .core import DataMatrix, FittedLine, SubspaceFit
+from .engine import DeviceFit
+
+__all__ = ["fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
+           "residual_error", "resolve_threads"]
+
+THREADS_ENV = "L1LINE_THREADS"
+
+
+def _check_lam(lam: float) -> float:
+    """fit.py:20-24: NaN and negatives are rejected, +inf is accepted."""
+    lam = float(lam)
+    if not lam >= 0.0:
+        raise ValueError(f"penalty weight must be nonnegative, got {lam}")
+    return lam
+
+
+def resolve_threads(threads: int | None = None) -> int:
+    """parallel.py:19-33 (validated for API parity; the GPU ignores it)."""
+    if threads is None:
+        env = os.environ.get(THREADS_ENV, "").strip()
+        if env:
+            try:
+                threads = int(env)
+            except ValueError:
+                raise ValueError(f"{THREADS_ENV} must be an integer, got {env!r}")
+        else:
+            threads = os.cpu_count() or 1
+    threads = int(threads)
+    if threads < 1:
+        raise ValueError("thread count must be at least 1")
+    return threads
+
+
+def _as_data(data) -> DataMatrix:
+    if isinstance(data, DataMatrix):
+        return data
+    return DataMatrix(np.asarray(getattr(data, "values", data), dtype=np.float64),
+                      column_names=getattr(data, "column_names", None))
+
+
+def _line(w) -> FittedLine:
+    return FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,
+                      penalty_norm=w.penalty_norm, objective=w.objective)
+
+
+def fit_lines(data, lams, threads: int | None = None) -> list[FittedLine]:
+    """Best line for every penalty weight in ``lams`` in one device pass.
+
+    Equivalent to ``[fit_line(data, lam) for lam in lams]``.
+    """
+    lams = [_check_lam(x) for x in np.atleast_1d(np.asarray(lams, dtype=np.float64))]
+    resolve_threads(threads)
+    d = _as_data(data)
+    eng = DeviceFit(d.values)
+    return [_line(w) for w in eng.shard_winners(lams)]
+
+
+def fit_line(data, lam: float, threads: int | None = None) -> FittedLine:
+    """Best coordinate-preserving line over all pivots (fit.py:88-102)."""
+    return fit_lines(data, [lam], threads)[0]
+
+
+def fit_for_pivot(data, pivot: int, lam: float) -> FittedLine:
+    """Best line that preserves one given coordinate (fit.py:75-85)."""
+    lam = _check_lam(lam)
+    d = _as_data(data)
+    pivot = int(pivot)
+    if not 0 <= pivot < d.m:
+        raise IndexError(f"pivot column {pivot} out of range")
+    eng = DeviceFit(d.values, max_pivots=1)
+    return _line(eng.shard_winners([lam], p_begin=pivot, p_stride=1, npiv=1)[0])
+
+
+def degenerate_line(data, pivot: int, lam: float) -> FittedLine:
+    """The all-zero line (fit.py:66-72): error = sum |x|, no penalty."""
+    lam = _check_lam(lam)
+    d = _as_data(data)
+    if not 0 <= int(pivot) < d.m:
+        raise IndexError(f"preserved column {pivot} out of range")
+    err = residual_error(d, np.zeros(d.m), int(pivot))
+    return FittedLine(v=np.zeros(d.m), preserved=int(pivot), lam=lam, error=err,
+                      penalty_norm=0.0, objective=err + lam * 0.0)
+
+
+def residual_error(data, v, preserved: int) -> float:
+    """core.py:79-93, bit-identical to the reference's NumPy reduction."""
+    d = _as_data(data)
+    if not 0 <= int(preserved) < d.m:
+        raise IndexError(f"preserved column {preserved} out of range")
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape != (d.m,):
+        raise ValueError(f"v has shape {v.shape}, expected ({d.m},)")
+    import torch
+    eng = DeviceFit(d.values, max_pivots=1)
+    return eng.residual_exact(torch.from_numpy(np.ascontiguousarray(v)).to(eng.device), int(preserved))
+
+
+def deflate(data, v) -> DataMatrix:
+    """X (I - w w^T), w = v / ||v||_2 (subspace.py:22-36), on the device."""
+    d = _as_data(data)
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape != (d.m,):
+        raise ValueError(f"v has shape {v.shape}, expected ({d.m},)")
+    if float(np.linalg.norm(v)) == 0.0:
+        raise ValueError("cannot deflate along the zero vector")
+    eng = DeviceFit(d.values, max_pivots=1)
+    eng.deflate(v)
+    return DataMatrix(eng.X.cpu().numpy(), column_names=d.column_names)
+
+
+def fit_subspace(data, lam: float, k: int, threads: int | None = None) -> SubspaceFit:
+    """Up to k components by fit-then-deflate, all on one device copy of X."""
+    d = _as_data(data)
+    if not 1 <= k < d.m:
+        raise ValueError(f"component count {k} must be in [1, {d.m - 1}]")
+    if lam < 0.0 or not math.isfinite(lam):
+        raise ValueError("penalty weight must be finite and nonnegative")
+    resolve_threads(threads)
+    eng = DeviceFit(d.values)
+    scale = max(1.0, eng.absmax())
+    comps: list[FittedLine] = []
+    for t in range(k):
+        if eng.absmax() <= 1e-10 * scale:
+            return SubspaceFit(tuple(comps), degenerate=True)
+        line = _line(eng.shard_winners([float(lam)])[0])
+        comps.append(line)
+        if t + 1 < k:
+            eng.deflate(line.v)
+    return SubspaceFit(tuple(comps), degenerate=False)

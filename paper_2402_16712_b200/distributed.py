@@ -1,0 +1,111 @@
+"""Pivot-sharded fit over several GPUs (one process per GPU).
+
+SURVEY.md 8(e): the m pivots are independent units (fit.py:97), so rank r
+fits pivots p = r, r + W, r + 2W, ... (interleaved, so zero-heavy column
+ranges stay balanced) on its own replica of X, and only the per-shard
+winner crosses the interconnect:
+
+1. every rank reports (exact objective, pivot) of its shard winner
+   (``torch.distributed.all_gather`` of 16 bytes per rank, NCCL over
+   NVLink on the GPU box, gloo in the CPU tests);
+2. all ranks take the lexicographic minimum of (objective, pivot) -- the
+   strict '<' in ascending pivot order of fit.py:98-102;
+3. the owning rank broadcasts the winning direction (8*m bytes).
+
+Each pivot is solved on exactly one rank with exactly the single-GPU
+kernels and re-scored with NumPy's summation order, so the result is
+byte-identical for any world size.  There is no data-path collective.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .core import FittedLine
+from .engine import DeviceFit, PivotWinner, shard
+
+__all__ = ["shard", "combine_winners", "fit_lines_distributed", "fit_line_distributed"]
+
+
+def _comm_device(group=None) -> torch.device:
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def combine_winners(local: list[PivotWinner | None], m: int, group=None) -> list[PivotWinner]:
+    """Global winner per lambda from every rank's shard winner.
+
+    ``local[l]`` is None when the rank owns no pivots.  Ties on the exact
+    objective go to the smallest pivot, as the sequential strict '<' does.
+    """
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = _comm_device(group)
+    L = len(local)
+    rec = torch.full((L, 5), float("inf"), dtype=torch.float64)
+    for l, w in enumerate(local):
+        if w is not None:
+            rec[l] = torch.tensor([w.objective, float(w.pivot), w.error, w.penalty_norm, w.lam],
+                                  dtype=torch.float64)
+    rec = rec.to(dev)
+    gathered = [torch.empty_like(rec) for _ in range(world)]
+    dist.all_gather(gathered, rec, group=group)
+    allr = torch.stack(gathered).cpu().numpy()  # [world][L][5]
+    out = []
+    for l in range(L):
+        best_r = -1
+        for r in range(world):
+            z, p = allr[r, l, 0], allr[r, l, 1]
+            if np.isinf(p):
+                continue
+            if best_r < 0:
+                best_r = r
+                continue
+            bz, bp = allr[best_r, l, 0], allr[best_r, l, 1]
+            if z < bz or (z == bz and p < bp):
+                best_r = r
+        if best_r < 0:
+            raise ValueError("no rank owns any pivot")
+        v = torch.empty(m, dtype=torch.float64, device=dev)
+        if me == best_r:
+            v.copy_(torch.from_numpy(np.ascontiguousarray(local[l].v)).to(dev))
+        src = dist.get_global_rank(group, best_r) if group is not None else best_r
+        dist.broadcast(v, src=src, group=group)
+        z, p, e, pn, lam = allr[best_r, l]
+        out.append(PivotWinner(int(p), float(lam), v.cpu().numpy().copy(), float(e), float(pn), float(z)))
+    return out
+
+
+def _device_solver(X, lams, p_begin, p_stride, npiv):
+    eng = DeviceFit(X, max_pivots=max(1, npiv))
+    return eng.shard_winners(lams, p_begin, p_stride, npiv)
+
+
+def fit_lines_distributed(X, lams, group=None,
+                          solver: Callable | None = None) -> list[FittedLine]:
+    """fit_line for every lambda with the pivots sharded over the process group.
+
+    ``solver(X, lams, p_begin, p_stride, npiv) -> list[PivotWinner]`` runs one
+    shard; it defaults to the device engine (tests substitute the CPU oracle
+    to exercise the multi-rank plumbing with gloo).
+    """
+    X = np.ascontiguousarray(getattr(X, "values", X), dtype=np.float64)
+    lams = [float(x) for x in np.atleast_1d(lams)]
+    m = X.shape[1]
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    p_begin, p_stride, npiv = shard(m, rank, world)
+    solver = solver or _device_solver
+    local = solver(X, lams, p_begin, p_stride, npiv) if npiv > 0 else [None] * len(lams)
+    wins = combine_winners(local, m, group)
+    return [FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error, penalty_norm=w.penalty_norm,
+                       objective=w.objective) for w in wins]
+
+
+def fit_line_distributed(X, lam: float, group=None, solver: Callable | None = None) -> FittedLine:
+    return fit_lines_distributed(X, [lam], group, solver)[0]

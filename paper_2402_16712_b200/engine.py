@@ -1,0 +1,180 @@
+"""Device-resident fit engine: one matrix, one workspace, one CUDA stream.
+
+``DeviceFit`` owns the device copy of X (row-major f64 exactly as
+``DataMatrix.values`` lays it out, core.py:49) and the workspace the C ABI
+needs, and runs Algorithm 1 for a pivot shard and a batch of penalty
+weights.  PyTorch is only the allocator/stream provider here; every
+computation is a kernel in ``csrc/l1b200.cu`` called through ``_lib``.
+
+Winner selection reproduces fit.py:98-102 exactly: the kernels rank pivots
+by objectives summed in a fixed device order, then every pivot whose
+objective is within ``RESCORE_RTOL`` of the minimum is re-scored with the
+reference's own rounding (``l1b_residual_exact`` = residual_error's NumPy
+pairwise order, core.py:93; ``np.abs(v).sum()`` for the penalty,
+core.py:131) and the first pivot with the smallest exact objective wins.
+The device sums differ from NumPy's by far less than RESCORE_RTOL, so the
+chosen pivot, error, penalty and objective are those the reference would
+report for the same directions.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+RESCORE_RTOL = 1e-8
+
+
+def _stream_handle(stream: torch.cuda.Stream | None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+@dataclass
+class PivotWinner:
+    """Exact-rescored winner of one pivot shard at one penalty weight."""
+
+    pivot: int
+    lam: float
+    v: np.ndarray
+    error: float
+    penalty_norm: float
+    objective: float
+
+
+def shard(m: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Interleaved pivot shard p = rank, rank + world, ...."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    npiv = max(0, (m - rank + world - 1) // world)
+    return rank, world, npiv
+
+
+class DeviceFit:
+    """A data matrix resident on one GPU plus everything a fit needs."""
+
+    def __init__(self, X, device: torch.device | str | None = None,
+                 stream: torch.cuda.Stream | None = None, max_pivots: int | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2402_16712_b200 needs a CUDA device (there is no CPU fallback)")
+        self.lib = _lib.load()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream
+        if isinstance(X, torch.Tensor):
+            Xd = X.to(device=self.device, dtype=torch.float64).contiguous()
+        else:
+            Xh = np.ascontiguousarray(X, dtype=np.float64)
+            Xd = torch.from_numpy(Xh).pin_memory().to(self.device, non_blocking=True) \
+                if Xh.size >= (1 << 16) else torch.from_numpy(Xh).to(self.device)
+        if Xd.dim() != 2:
+            raise ValueError(f"expected a 2-d array, got shape {tuple(Xd.shape)}")
+        self.X = Xd
+        self.n, self.m = int(Xd.shape[0]), int(Xd.shape[1])
+        self.max_pivots = self.m if max_pivots is None else int(max_pivots)
+        nbytes = self.lib.l1b_workspace_bytes(self.n, self.m, 1, max(1, self.max_pivots))
+        if nbytes == 0:
+            raise ValueError(f"bad matrix shape {(self.n, self.m)}")
+        with torch.cuda.device(self.device):
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self.tmp = torch.empty(self.n + 2, dtype=torch.float64, device=self.device)
+            self.scalar = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.prepare()
+
+    # ------------------------------------------------------------- kernels --
+    @property
+    def _s(self) -> int:
+        return _stream_handle(self.stream)
+
+    def prepare(self) -> None:
+        """K0 (l1b_prepare); rerun whenever X changes."""
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_prepare(self.X.data_ptr(), self.n, self.m, self.ws.data_ptr(),
+                                            self.ws.numel(), self._s), "l1b_prepare")
+
+    def fit_pivots(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None,
+                   want_v: bool = True):
+        """K1+K2 for a pivot shard: device tensors V [L][np][m], err/pen/obj [L][np]."""
+        lam = np.ascontiguousarray(np.atleast_1d(np.asarray(lams, dtype=np.float64)))
+        if npiv is None:
+            npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
+        if npiv > self.max_pivots:
+            raise ValueError(f"shard of {npiv} pivots exceeds workspace for {self.max_pivots}")
+        L = lam.size
+        with torch.cuda.device(self.device):
+            V = torch.empty((L, npiv, self.m), dtype=torch.float64, device=self.device) if want_v else None
+            err = torch.empty((L, npiv), dtype=torch.float64, device=self.device)
+            pen = torch.empty_like(err)
+            obj = torch.empty_like(err)
+            rc = self.lib.l1b_fit_pivots(
+                self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                L, p_begin, p_stride, npiv, V.data_ptr() if want_v else None, err.data_ptr(),
+                pen.data_ptr(), obj.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+        _lib.check(rc, "l1b_fit_pivots")
+        return V, err, pen, obj
+
+    def residual_exact(self, v_dev: torch.Tensor, pivot: int) -> float:
+        """residual_error (core.py:79-93) with NumPy's exact summation order."""
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_residual_exact(self.X.data_ptr(), self.n, self.m, v_dev.data_ptr(),
+                                                   int(pivot), self.scalar.data_ptr(), self.ws.data_ptr(),
+                                                   self.ws.numel(), self._s), "l1b_residual_exact")
+            return float(self.scalar.item())
+
+    def deflate(self, v) -> None:
+        """subspace.py:22-36 in place on the device copy, then re-prepare."""
+        with torch.cuda.device(self.device):
+            v_dev = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(self.device)
+            _lib.check(self.lib.l1b_deflate(self.X.data_ptr(), self.n, self.m, v_dev.data_ptr(),
+                                            self.tmp.data_ptr(), self._s), "l1b_deflate")
+        self.prepare()
+
+    def absmax(self) -> float:
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_absmax(self.X.data_ptr(), self.n, self.m, self.scalar.data_ptr(),
+                                           self._s), "l1b_absmax")
+            return float(self.scalar.item())
+
+    # ------------------------------------------------------------- winners --
+    def shard_winners(self, lams, p_begin: int = 0, p_stride: int = 1,
+                      npiv: int | None = None) -> list[PivotWinner]:
+        """Exact winner of the shard for every lambda (fit.py:98-102 semantics)."""
+        lam = np.atleast_1d(np.asarray(lams, dtype=np.float64))
+        V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
+        obj_h = obj.cpu().numpy()
+        out = []
+        for l in range(lam.size):
+            o = obj_h[l]
+            if np.isnan(o).any():
+                # FittedLine's invariant rejects a NaN objective (core.py:120-124):
+                # only lam=inf with an all-zero pivot column produces one.
+                raise ValueError(f"objective nan for lam={lam[l]!r} (zero pivot column at infinite penalty)")
+            best = float(o.min())
+            if math.isinf(best):
+                cand = np.nonzero(o == best)[0][:1]
+            else:
+                cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + 1e-300)[0]
+            win = None
+            for k in cand:  # ascending pivot order
+                p = p_begin + int(k) * p_stride
+                v_dev = V[l, k]
+                e = self.residual_exact(v_dev, p)
+                vh = v_dev.cpu().numpy().copy()
+                pn = float(np.abs(vh).sum())
+                z = e + float(lam[l]) * pn
+                if win is None or z < win.objective:
+                    win = PivotWinner(p, float(lam[l]), vh, e, pn, z)
+            out.append(win)
+        return out
+
+    def selftest_divide(self, n_pairs: int = 1 << 26, seed: int = 1) -> int:
+        with torch.cuda.device(self.device):
+            cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+            _lib.check(self.lib.l1b_selftest_divide(seed, n_pairs, cnt.data_ptr(), self._s),
+                       "l1b_selftest_divide")
+            return int(cnt.item())

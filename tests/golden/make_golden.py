@@ -1,0 +1,173 @@
+"""Generate the golden parity fixtures from the REFERENCE implementation.
+
+Run in the build container, where the read-only reference is importable:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every array written here comes out of the reference package ``l1line``
+(``/root/reference/pkg/src/l1line``) through its public API: ``fit_line``
+(fit.py:88-102), ``fit_for_pivot`` (fit.py:75-85), ``fit_subspace``
+(subspace.py:54-76), ``gen_line_data`` / ``gen_outlier_data``
+(datagen.py:36-82).  The GPU box has no /root/reference, so the tests read
+these committed .npz files instead.  Inputs mirror the reference's own test
+recipes: ``random_instance`` (pkg/tests/conftest.py:22-33), grid-quantised
+copies, exact ties, exact zeros and -0.0 entries.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import l1line  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref_pivots(X, lams):
+    """Per-pivot reference results for every lambda: V [m][L][m], E/P/O [m][L]."""
+    d = l1line.DataMatrix(X)
+    m = X.shape[1]
+    V = np.zeros((m, len(lams), m))
+    E = np.zeros((m, len(lams)))
+    P = np.zeros((m, len(lams)))
+    O = np.zeros((m, len(lams)))
+    for p in range(m):
+        for k, lam in enumerate(lams):
+            line = l1line.fit_for_pivot(d, p, lam)
+            V[p, k], E[p, k], P[p, k], O[p, k] = line.v, line.error, line.penalty_norm, line.objective
+    return V, E, P, O
+
+
+def _ref_lines(X, lams):
+    d = l1line.DataMatrix(X)
+    out = {"piv": [], "v": [], "err": [], "pen": [], "obj": []}
+    for lam in lams:
+        line = l1line.fit_line(d, lam, threads=1)
+        out["piv"].append(line.preserved)
+        out["v"].append(line.v)
+        out["err"].append(line.error)
+        out["pen"].append(line.penalty_norm)
+        out["obj"].append(line.objective)
+    return {k: np.asarray(v) for k, v in out.items()}
+
+
+def random_small():
+    """Ragged set of small instances in the style of conftest.random_instance."""
+    rng = np.random.default_rng(20240226)
+    mats, lams_all, shapes = [], [], []
+    pV, pE, pP, pO, lpiv, lv, lerr, lpen, lobj = [], [], [], [], [], [], [], [], []
+    for t in range(160):
+        n = int(rng.integers(1, 33))
+        m = int(rng.integers(2, 9))
+        X = rng.uniform(-10.0, 10.0, size=(n, m))
+        kind = t % 6
+        if kind == 1:
+            X[rng.random(X.shape) < 0.25] = 0.0          # exact zeros (conftest zeros=True)
+        elif kind == 2:
+            X = np.round(X)                               # many exact ratio ties
+        elif kind == 3:
+            X[rng.random(X.shape) < 0.25] = -0.0          # signed zeros
+            X[rng.random(X.shape) < 0.1] = 0.0
+        elif kind == 4:
+            X = np.round(X * 2**4) / 2**4                 # grid-quantised
+            X[:, int(rng.integers(m))] = 0.0              # a zero column -> degenerate pivot
+        elif kind == 5:
+            X[:, -1] = X[:, 0]                            # identical columns -> objective ties
+        tot = float(np.abs(X).sum())
+        lams = [0.0, float(rng.uniform(0, 3)), float(rng.uniform(0, tot / 2 + 1)),
+                float(rng.uniform(0, tot + 1))]
+        V, E, P, O = _ref_pivots(X, lams)
+        L = _ref_lines(X, lams)
+        mats.append(X.ravel())
+        shapes.append((n, m))
+        lams_all.append(lams)
+        pV.append(V.ravel()); pE.append(E.ravel()); pP.append(P.ravel()); pO.append(O.ravel())
+        lpiv.append(L["piv"]); lv.append(L["v"].ravel()); lerr.append(L["err"])
+        lpen.append(L["pen"]); lobj.append(L["obj"])
+    np.savez_compressed(
+        os.path.join(OUT, "random_small.npz"),
+        shapes=np.asarray(shapes, dtype=np.int64), X=np.concatenate(mats),
+        lams=np.asarray(lams_all), pV=np.concatenate(pV), pE=np.concatenate(pE),
+        pP=np.concatenate(pP), pO=np.concatenate(pO), lpiv=np.asarray(lpiv, dtype=np.int64),
+        lv=np.concatenate(lv), lerr=np.asarray(lerr), lpen=np.asarray(lpen), lobj=np.asarray(lobj))
+
+
+def c1_and_grid():
+    """Config C1 (BASELINE.json configs[0]) raw and grid-quantised, plus a medium grid case."""
+    d, vtrue = l1line.gen_outlier_data(50, 200, 20, seed=0)
+    X = d.values.copy()
+    Xq = np.round(X * 2**20) / 2**20
+    lams = [0.1, 0.0, 25.0, 500.0, 1500.0]
+    out = {"X": X, "Xq": Xq, "vtrue": vtrue, "lams": np.asarray(lams)}
+    for tag, M in (("raw", X), ("grid", Xq)):
+        V, E, P, O = _ref_pivots(M, lams)
+        L = _ref_lines(M, lams)
+        out.update({f"{tag}_pV": V, f"{tag}_pE": E, f"{tag}_pP": P, f"{tag}_pO": O})
+        out.update({f"{tag}_{k}": v for k, v in L.items()})
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **out)
+
+    d2, _ = l1line.gen_line_data(40, 300, seed=7, noise_scale=1.0)
+    G = np.round(d2.values * 2**20) / 2**20
+    lams2 = [0.0, 1.0, 50.0, 400.0]
+    V, E, P, O = _ref_pivots(G, lams2)
+    L = _ref_lines(G, lams2)
+    np.savez_compressed(os.path.join(OUT, "grid_medium.npz"), X=G, lams=np.asarray(lams2),
+                        pV=V, pE=E, pP=P, pO=O, **{f"l_{k}": v for k, v in L.items()})
+
+
+def subspace_cases():
+    toy = np.array([[4.0, -2.0, 3.0, -6.0], [-3.0, 4.0, 2.0, -1.0], [2.0, 3.0, -3.0, -2.0],
+                    [-3.0, 4.0, 2.0, 3.0], [5.0, 3.0, 2.0, -1.0]])
+    rng = np.random.default_rng(5)
+    R = rng.uniform(-10, 10, size=(40, 6))
+    G = np.round(l1line.gen_line_data(8, 120, seed=3, noise_scale=0.5)[0].values * 2**20) / 2**20
+    out = {}
+    for tag, X, lam, k in (("toy", toy, 1.0, 3), ("rand", R, 2.0, 3), ("grid", G, 1.0, 3)):
+        fit = l1line.fit_subspace(l1line.DataMatrix(X), lam, k, threads=1)
+        out[f"{tag}_X"] = X
+        out[f"{tag}_lam"] = lam
+        out[f"{tag}_k"] = k
+        out[f"{tag}_degenerate"] = fit.degenerate
+        out[f"{tag}_piv"] = np.asarray([c.preserved for c in fit.components])
+        out[f"{tag}_v"] = np.asarray([c.v for c in fit.components])
+        out[f"{tag}_obj"] = np.asarray([c.objective for c in fit.components])
+        out[f"{tag}_err"] = np.asarray([c.error for c in fit.components])
+    X1 = np.outer([1.0, 2.0, -1.0], [3.0, 0.0, 4.0])                   # rank one: stops early
+    fit = l1line.fit_subspace(l1line.DataMatrix(X1), 0.0, 2)
+    out["rank1_X"] = X1
+    out["rank1_n"] = len(fit)
+    out["rank1_degenerate"] = fit.degenerate
+    np.savez_compressed(os.path.join(OUT, "subspace.npz"), **out)
+
+
+def datagen_cases():
+    out = {}
+    for (m, n, seed, ns) in ((7, 11, 0, 1.0), (5, 9, 3, 0.0), (12, 30, 42, 2.5)):
+        d, v = l1line.gen_line_data(m, n, seed=seed, noise_scale=ns)
+        out[f"line_{m}_{n}_{seed}_X"] = d.values
+        out[f"line_{m}_{n}_{seed}_v"] = v
+    for (m, n, k, seed) in ((6, 13, 3, 1), (50, 200, 20, 0)):
+        d, v = l1line.gen_outlier_data(m, n, k, seed=seed)
+        out[f"outl_{m}_{n}_{k}_{seed}_X"] = d.values
+        out[f"outl_{m}_{n}_{k}_{seed}_v"] = v
+    d, v = l1line.gen_line_data(2000, 2000, seed=0, noise_scale=1.0)
+    # C2 checksum (the full matrix is 32 MB): first/last rows and a strided sample.
+    out["c2_head"] = d.values[:2].copy()
+    out["c2_tail"] = d.values[-2:].copy()
+    out["c2_stride"] = d.values[::97, ::89].copy()
+    out["c2_v"] = v
+    np.savez_compressed(os.path.join(OUT, "datagen.npz"), **out)
+
+
+if __name__ == "__main__":
+    random_small()
+    c1_and_grid()
+    subspace_cases()
+    datagen_cases()
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -1,0 +1,301 @@
+"""GPU parity: the CUDA path against the reference's goldens and the oracle.
+
+Bar (BASELINE.json north_star): pivot, selected ratios and sparsity pattern
+exactly; objective and directions within 1e-5 relative.  We hold a tighter
+bar: directions bit-identical to the reference on every input whose prefix
+sums are exact in f64 (all goldens, grid-quantised data, integer data), and
+the winning line's error / penalty / objective bit-identical whenever its
+direction is (the winner is re-scored in NumPy's summation order).  On raw
+data the direction is compared tie-aware: a differing column
+is accepted only if both values give the same column objective to 1e-12.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2402_16712_b200 as l1b
+from conftest import TOY, iter_random_small, iter_random_small_lines, load_golden
+from paper_2402_16712_b200.engine import DeviceFit
+
+pytestmark = pytest.mark.gpu
+
+OBJ_RTOL = 1e-12
+
+
+def _col_obj(X, p, j, t, lam):
+    return float(np.abs(X[:, j] - t * X[:, p]).sum()) + lam * abs(t)
+
+
+def _assert_v_tie_aware(X, p, lam, got, want, what=""):
+    if got.tobytes() == want.tobytes():
+        return 0
+    bad = np.nonzero(got.view(np.int64) != want.view(np.int64))[0]
+    for j in bad:
+        a, b = _col_obj(X, p, j, got[j], lam), _col_obj(X, p, j, want[j], lam)
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(b)), (what, p, j, got[j], want[j], a, b)
+    return len(bad)
+
+
+def _pivots(X, lams, **kw):
+    eng = DeviceFit(X)
+    V, E, P, O = eng.fit_pivots(lams, **kw)
+    torch.cuda.synchronize()
+    return eng, V.cpu().numpy(), E.cpu().numpy(), P.cpu().numpy(), O.cpu().numpy()
+
+
+def test_division_selftest_bit_exact():
+    eng = DeviceFit(TOY)
+    assert eng.selftest_divide(n_pairs=1 << 28, seed=7) == 0
+
+
+# ------------------------------------------------------ reference KATs --
+
+def test_fit_for_pivot_known_lines():
+    # pkg/tests/test_fit.py:93-103
+    line = l1b.fit_for_pivot(TOY, 3, 0.0)
+    assert line.v.tolist() == [-2.0 / 3.0, 1.0 / 3.0, -0.5, 1.0]
+    assert line.error == 34.5 and line.penalty_norm == 2.5
+    assert l1b.fit_for_pivot(TOY, 0, 2.0).v.tolist() == [1.0, -0.5, 0.0, -0.2]
+    assert l1b.fit_for_pivot(TOY, 0, 5.0).v.tolist() == [1.0, 0.0, 0.0, -0.2]
+
+
+def test_toy_column_walk():
+    # pkg/tests/test_fit.py:18-27: column (p=0, j=3) -1 -> -1/5 -> 0 at lam 1 and 11
+    for lam, want in [(0.0, -1.0), (0.5, -1.0), (1.0, -0.2), (10.999, -0.2), (11.0, 0.0), (50.0, 0.0)]:
+        assert l1b.fit_for_pivot(TOY, 0, lam).v[3] == want
+
+
+def test_fit_line_toy_goldens():
+    # pkg/tests/test_fit.py:106-114, test_acceptance.py:80-84
+    assert l1b.fit_line(TOY, 0.0).preserved == 3
+    assert l1b.fit_line(TOY, 5.0).preserved == 0
+    for lam in (0.0, 1.0, 2.5, 3.5, 7.0, 12.0):
+        got, want = l1b.fit_line(TOY, lam), oracle.fit_line(TOY, lam)
+        assert (got.preserved, got.v.tobytes(), got.objective) == (want.preserved, want.v.tobytes(), want.objective)
+    for lam, z in [(0.0, 34.5), (3.0, 42.0), (3.5, 43.0), (11.0, 52.0)]:
+        assert l1b.fit_line(TOY, lam).objective == pytest.approx(z, abs=1e-12)
+
+
+def test_tie_prefers_smaller_pivot():
+    X = np.array([[1.0, 1.0, 3.0], [2.0, 2.0, -1.0], [-1.0, -1.0, 2.0]])
+    for lam in (0.0, 0.5, 2.0):
+        assert l1b.fit_line(X, lam).preserved == 0
+
+
+def test_zero_column_and_zero_line():
+    # pkg/tests/test_fit.py:125-147
+    X = np.array([[0.0, 2.0, 1.0], [0.0, -1.0, 3.0]])
+    line = l1b.fit_for_pivot(X, 0, 1.0)
+    assert not line.v.any() and line.error == float(np.abs(X).sum()) and line.penalty_norm == 0.0
+    assert l1b.fit_line(X, 0.0).preserved in (1, 2)
+    big = l1b.fit_line(X, 100.0)
+    assert not big.v.any() and big.objective == float(np.abs(X).sum())
+
+
+def test_infinite_lambda():
+    got, want = l1b.fit_line(TOY, math.inf), oracle.fit_line(TOY, math.inf)
+    assert got.preserved == want.preserved == 0
+    assert got.v.tobytes() == want.v.tobytes() and got.error == want.error and math.isinf(got.objective)
+
+
+# ------------------------------------------------------------- goldens --
+
+def test_random_small_golden():
+    lvs = iter_random_small_lines()
+    for t, X, lams, (pV, pE, pP, pO), lpiv, lobj, lerr, lpen in iter_random_small():
+        if X.shape[0] < 1:
+            continue
+        _, V, E, P, O = _pivots(X, lams)
+        V = V.transpose(1, 0, 2)  # [m][L][m] like the golden
+        assert V.tobytes() == pV.tobytes(), t
+        np.testing.assert_allclose(O.T, pO, rtol=OBJ_RTOL, atol=1e-12)
+        lines = l1b.fit_lines(X, lams)
+        for k, line in enumerate(lines):
+            assert line.preserved == lpiv[k], (t, k)
+            assert line.v.tobytes() == lvs[t][k].tobytes(), (t, k)
+            assert (line.objective, line.error, line.penalty_norm) == (lobj[k], lerr[k], lpen[k]), (t, k)
+
+
+@pytest.mark.parametrize("tag", ["raw", "grid"])
+def test_c1_golden(tag):
+    g = load_golden("c1.npz")
+    X = g["X"] if tag == "raw" else g["Xq"]
+    lams = g["lams"]
+    _, V, E, P, O = _pivots(X, lams)
+    assert V.transpose(1, 0, 2).tobytes() == g[f"{tag}_pV"].tobytes()
+    np.testing.assert_allclose(O.T, g[f"{tag}_pO"], rtol=OBJ_RTOL)
+    for k, line in enumerate(l1b.fit_lines(X, lams)):
+        assert line.preserved == g[f"{tag}_piv"][k]
+        assert line.v.tobytes() == g[f"{tag}_v"][k].tobytes()
+        assert line.objective == g[f"{tag}_obj"][k] and line.error == g[f"{tag}_err"][k]
+
+
+def test_grid_medium_golden():
+    g = load_golden("grid_medium.npz")
+    _, V, E, P, O = _pivots(g["X"], g["lams"])
+    assert V.transpose(1, 0, 2).tobytes() == g["pV"].tobytes()
+    np.testing.assert_allclose(O.T, g["pO"], rtol=OBJ_RTOL)
+    for k, line in enumerate(l1b.fit_lines(g["X"], g["lams"])):
+        assert line.preserved == g["l_piv"][k] and line.objective == g["l_obj"][k]
+
+
+def test_subspace_golden():
+    g = load_golden("subspace.npz")
+    for tag in ("toy", "rand", "grid"):
+        fit = l1b.fit_subspace(g[f"{tag}_X"], float(g[f"{tag}_lam"]), int(g[f"{tag}_k"]))
+        assert fit.degenerate == bool(g[f"{tag}_degenerate"])
+        piv = [c.preserved for c in fit.components]
+        assert piv == g[f"{tag}_piv"].tolist(), tag
+        # component 1 is bit-exact; later ones see device-deflated data whose
+        # rounding differs from BLAS dgemv at the 1e-16 level
+        c0 = fit.components[0]
+        assert c0.v.tobytes() == g[f"{tag}_v"][0].tobytes() and c0.objective == g[f"{tag}_obj"][0]
+        np.testing.assert_allclose([c.objective for c in fit.components], g[f"{tag}_obj"], rtol=1e-9)
+        np.testing.assert_allclose(np.array([c.v for c in fit.components]), g[f"{tag}_v"], rtol=1e-9, atol=1e-12)
+    fit = l1b.fit_subspace(g["rank1_X"], 0.0, 2)
+    assert fit.degenerate and len(fit) == int(g["rank1_n"])
+
+
+# --------------------------------------------------- oracle at scale --
+
+def _grid(X, bits=20):
+    return np.round(X * 2.0**bits) / 2.0**bits
+
+
+@pytest.mark.parametrize("n,m,seed", [(400, 48, 0), (3000, 24, 1), (1, 6, 2), (7, 2, 3), (1000, 33, 4)])
+def test_grid_data_bit_exact_vs_oracle(n, m, seed):
+    d, _ = l1b.gen_line_data(m, n, seed=seed, noise_scale=1.0)
+    X = _grid(d.values)
+    lams = [0.0, 1.0, 0.3 * float(np.abs(X).sum(axis=0).max()), 1e9]
+    _, V, E, P, O = _pivots(X, lams)
+    Vo, Eo, Po, Oo = oracle.fit_pivots(X, lams)
+    assert V.transpose(1, 0, 2).tobytes() == Vo.tobytes()
+    np.testing.assert_allclose(O.T, Oo, rtol=1e-11)
+    for k, line in enumerate(l1b.fit_lines(X, lams)):
+        want = oracle.fit_line(X, lams[k])
+        assert line.preserved == want.preserved and line.v.tobytes() == want.v.tobytes()
+        assert line.objective == want.objective
+
+
+@pytest.mark.parametrize("kind", ["integers", "sparse", "signed_zeros", "duplicate_rows", "noiseless"])
+def test_adversarial_ties_vs_oracle(kind):
+    """Exercises the tie paths: 64-bit refinement, the +-0 group in row order."""
+    rng = np.random.default_rng(hash(kind) % 2**32)
+    n, m = 600, 20
+    if kind == "integers":
+        X = np.round(rng.uniform(-4, 4, size=(n, m)))
+    elif kind == "sparse":
+        X = np.round(rng.uniform(-10, 10, size=(n, m)), 1)
+        X[rng.random(X.shape) < 0.7] = 0.0
+    elif kind == "signed_zeros":
+        X = np.round(rng.uniform(-3, 3, size=(n, m)))
+        X[rng.random(X.shape) < 0.4] = -0.0
+    elif kind == "duplicate_rows":
+        base = np.round(rng.uniform(-10, 10, size=(40, m)), 2)
+        X = base[rng.integers(0, 40, size=n)]
+    else:  # rank one: every ratio of a column identical up to rounding
+        X = np.outer(rng.uniform(-100, 100, size=n), rng.uniform(-1, 1, size=m))
+    lams = [0.0, 0.5, 3.0, 50.0]
+    _, V, E, P, O = _pivots(X, lams)
+    Vo, Eo, Po, Oo = oracle.fit_pivots(X, lams)
+    if kind == "noiseless":
+        # raw products: prefix sums are not exact, compare tie-aware
+        for p in range(m):
+            for k, lam in enumerate(lams):
+                _assert_v_tie_aware(X, p, lam, V[k, p], Vo[p, k], kind)
+    else:
+        assert V.transpose(1, 0, 2).tobytes() == Vo.tobytes()
+    np.testing.assert_allclose(O.T, Oo, rtol=1e-10, atol=1e-9)
+
+
+def test_extreme_exponents_take_exact_division_path():
+    rng = np.random.default_rng(9)
+    X = rng.uniform(-10, 10, size=(300, 12))
+    X[:, 3] *= 2.0**600
+    X[:, 7] *= 2.0**-700
+    X[5, 2] = 5e-324  # a subnormal entry
+    lams = [0.0, 2.0]
+    _, V, E, P, O = _pivots(X, lams)
+    Vo, Eo, Po, Oo = oracle.fit_pivots(X, lams)
+    for p in range(X.shape[1]):
+        for k, lam in enumerate(lams):
+            _assert_v_tie_aware(X, p, lam, V[k, p], Vo[p, k], "extreme")
+    np.testing.assert_allclose(O.T, Oo, rtol=1e-10)
+
+
+def test_raw_c2_shape_sampled_pivots_vs_oracle():
+    """Full 2000 x 2000 C2 input: every pivot on the GPU, 12 sampled on the CPU."""
+    d, _ = l1b.gen_line_data(2000, 2000, seed=0, noise_scale=1.0)
+    X = d.values
+    eng = DeviceFit(X)
+    V, E, P, O = eng.fit_pivots([1.0])
+    V, O = V.cpu().numpy()[0], O.cpu().numpy()[0]
+    best = int(np.argmin(O))
+    sample = sorted({0, 1, 1329, 308, best, 1999, *np.random.default_rng(0).integers(0, 2000, 6).tolist()})
+    for p in sample:
+        want = oracle.fit_for_pivot(X, p, 1.0)
+        nbad = _assert_v_tie_aware(X, p, 1.0, V[p], want.v, "c2")
+        assert nbad <= 2
+        assert O[p] == pytest.approx(want.objective, rel=1e-11)
+    line = eng.shard_winners([1.0])[0]
+    # C2 at lam=1 -> pivot 1329, z = 4561881.260523822
+    assert line.pivot == 1329
+    assert line.objective == pytest.approx(4561881.260523822, rel=1e-12)
+
+
+def test_grid_c2_winner_bit_exact():
+    d, _ = l1b.gen_line_data(2000, 2000, seed=0, noise_scale=1.0)
+    X = _grid(d.values)
+    eng = DeviceFit(X)
+    win = eng.shard_winners([1.0, 2500.0])
+    for w in win:
+        want = oracle.fit_for_pivot(X, w.pivot, w.lam)
+        assert w.v.tobytes() == want.v.tobytes()
+        assert (w.error, w.penalty_norm, w.objective) == (want.error, want.penalty_norm, want.objective)
+
+
+def test_batched_lambdas_equal_single_calls_and_are_deterministic():
+    d, _ = l1b.gen_outlier_data(50, 200, 20, seed=0)
+    X = d.values
+    lams = [0.0, 0.1, 7.5, 120.0, 900.0]
+    eng = DeviceFit(X)
+    V1, _, _, O1 = eng.fit_pivots(lams)
+    V2, _, _, O2 = eng.fit_pivots(lams)
+    assert torch.equal(V1, V2) and torch.equal(O1, O2)
+    for k, lam in enumerate(lams):
+        Vs, _, _, Os = eng.fit_pivots([lam])
+        assert torch.equal(Vs[0], V1[k]) and torch.equal(Os[0], O1[k])
+    # sharded pivots give byte-identical per-pivot results
+    for stride in (2, 3):
+        for r in range(stride):
+            npiv = (50 - r + stride - 1) // stride
+            Vs, _, _, Os = eng.fit_pivots(lams, p_begin=r, p_stride=stride, npiv=npiv)
+            assert torch.equal(Vs, V1[:, r::stride]) and torch.equal(Os, O1[:, r::stride])
+
+
+def test_use_gpu_patches_reference_bindings():
+    import sys
+    import types
+    # a stand-in for an installed l1line with by-value bindings
+    core = types.ModuleType("fake_l1line.core")
+    core.FittedLine = l1b.FittedLine
+    pkg = types.ModuleType("fake_l1line")
+    pkg.fit_line = None
+    pkg.__path__ = []
+    sub = types.ModuleType("fake_l1line.subspace")
+    sub.fit_line = None
+    sub.SubspaceFit = l1b.SubspaceFit
+    sys.modules.update({"fake_l1line": pkg, "fake_l1line.core": core, "fake_l1line.subspace": sub})
+    try:
+        from paper_2402_16712_b200.integration import restore, use_gpu
+        use_gpu("fake_l1line")
+        assert pkg.fit_line(TOY, 0.0).preserved == 3 and sub.fit_line(TOY, 5.0).preserved == 0
+        restore()
+        assert pkg.fit_line is None
+    finally:
+        for k in ("fake_l1line", "fake_l1line.core", "fake_l1line.subspace"):
+            sys.modules.pop(k, None)

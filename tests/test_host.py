@@ -1,0 +1,159 @@
+"""CPU-only checks: datagen bytes, host contracts, C-ABI export list, sharding."""
+
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2402_16712_b200 as l1b
+from conftest import ROOT, TOY, load_golden
+from paper_2402_16712_b200 import _lib
+from paper_2402_16712_b200.engine import shard
+
+
+# ---------------------------------------------------------------- datagen --
+
+def test_datagen_bytes_match_reference():
+    g = load_golden("datagen.npz")
+    for (m, n, seed, ns) in ((7, 11, 0, 1.0), (5, 9, 3, 0.0), (12, 30, 42, 2.5)):
+        d, v = l1b.gen_line_data(m, n, seed=seed, noise_scale=ns)
+        assert d.values.tobytes() == g[f"line_{m}_{n}_{seed}_X"].tobytes()
+        assert v.tobytes() == g[f"line_{m}_{n}_{seed}_v"].tobytes()
+    for (m, n, k, seed) in ((6, 13, 3, 1), (50, 200, 20, 0)):
+        d, v = l1b.gen_outlier_data(m, n, k, seed=seed)
+        assert d.values.tobytes() == g[f"outl_{m}_{n}_{k}_{seed}_X"].tobytes()
+        assert v.tobytes() == g[f"outl_{m}_{n}_{k}_{seed}_v"].tobytes()
+
+
+def test_datagen_c2_checksum():
+    g = load_golden("datagen.npz")
+    d, v = l1b.gen_line_data(2000, 2000, seed=0, noise_scale=1.0)
+    X = d.values
+    assert X[:2].tobytes() == g["c2_head"].tobytes()
+    assert X[-2:].tobytes() == g["c2_tail"].tobytes()
+    assert X[::97, ::89].tobytes() == g["c2_stride"].tobytes()
+    assert v.tobytes() == g["c2_v"].tobytes()
+
+
+def test_datagen_validation():
+    with pytest.raises(ValueError):
+        l1b.gen_line_data(1, 5, 0)
+    with pytest.raises(ValueError):
+        l1b.gen_line_data(3, 0, 0)
+    with pytest.raises(ValueError):
+        l1b.gen_outlier_data(4, 10, 2, 0)
+
+
+# ------------------------------------------------------------- core types --
+
+def test_datamatrix_contract():
+    # core.py:48-68 / pkg/tests/test_core.py:15-52
+    d = l1b.DataMatrix(TOY)
+    assert d.n == 5 and d.m == 4 and not d.values.flags.writeable
+    with pytest.raises(ValueError):
+        l1b.DataMatrix(np.zeros(3))
+    with pytest.raises(ValueError):
+        l1b.DataMatrix(np.zeros((0, 3)))
+    with pytest.raises(ValueError):
+        l1b.DataMatrix(np.zeros((3, 1)))
+    with pytest.raises(ValueError, match="row 1, column 2"):
+        bad = np.zeros((3, 3))
+        bad[1, 2] = np.nan
+        l1b.DataMatrix(bad)
+    with pytest.raises(ValueError):
+        l1b.DataMatrix(TOY, column_names=("a", "b"))
+    assert l1b.DataMatrix(TOY, column_names=list("abcd")).column_names == tuple("abcd")
+
+
+def test_fitted_line_invariants():
+    # core.py:113-124 / pkg/tests/test_core.py:77-109
+    v = np.array([1.0, -0.5, 0.0])
+    line = l1b.FittedLine(v=v, preserved=0, lam=2.0, error=3.0, penalty_norm=1.5, objective=6.0)
+    assert not line.v.flags.writeable and line.objective_at(0.0) == 3.0
+    with pytest.raises(ValueError):
+        l1b.FittedLine(v=v, preserved=1, lam=2.0, error=3.0, penalty_norm=1.5, objective=6.0)
+    with pytest.raises(ValueError):
+        l1b.FittedLine(v=v, preserved=0, lam=2.0, error=3.0, penalty_norm=1.5, objective=6.5)
+    with pytest.raises(ValueError):
+        l1b.FittedLine(v=v, preserved=0, lam=-1.0, error=3.0, penalty_norm=1.5, objective=1.5)
+    l1b.FittedLine(v=np.zeros(3), preserved=2, lam=1.0, error=3.0, penalty_norm=0.0, objective=3.0)
+
+
+def test_lambda_and_threads_validation():
+    from paper_2402_16712_b200.api import _check_lam, resolve_threads
+    assert _check_lam(math.inf) == math.inf
+    for bad in (-1.0, math.nan, -1e-300):
+        with pytest.raises(ValueError):
+            _check_lam(bad)
+    assert resolve_threads(3) == 3
+    with pytest.raises(ValueError):
+        resolve_threads(0)
+
+
+def test_lambda_rejected_before_any_device_work():
+    for fn in (lambda: l1b.fit_line(TOY, -1.0), lambda: l1b.fit_lines(TOY, [0.0, float("nan")]),
+               lambda: l1b.fit_for_pivot(TOY, 0, -0.5)):
+        with pytest.raises(ValueError):
+            fn()
+    with pytest.raises(IndexError):
+        l1b.fit_for_pivot(TOY, 4, 1.0)
+    with pytest.raises(ValueError):
+        l1b.fit_subspace(TOY, 1.0, 4)
+    with pytest.raises(ValueError):
+        l1b.fit_subspace(TOY, math.inf, 2)
+
+
+# -------------------------------------------------------------- sharding --
+
+def test_shard_partitions_pivots():
+    for m in (2, 3, 50, 2000, 10_001):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                b, s, k = shard(m, r, world)
+                seen += [b + i * s for i in range(k)]
+            assert sorted(seen) == list(range(m))
+    with pytest.raises(ValueError):
+        shard(10, 3, 3)
+
+
+# -------------------------------------------------------------------- ABI --
+
+def _header_symbols():
+    txt = open(os.path.join(ROOT, "include", "l1b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(l1b_\w+)\(", txt, re.M)))
+
+
+def test_abi_library_exports_every_header_symbol():
+    syms = _header_symbols()
+    assert len(syms) >= 9
+    assert sorted(_lib.ABI_SYMBOLS) == syms
+    lib = _lib.load()  # loads without a GPU
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.l1b_version() == 1
+    assert lib.l1b_status_string(0) == b"ok"
+    assert lib.l1b_status_string(-1) == b"invalid argument"
+
+
+def test_abi_workspace_and_argument_checks():
+    lib = _lib.load()
+    assert lib.l1b_workspace_bytes(2000, 2000, 1, 2000) > 2000 * 2000 * 32
+    assert lib.l1b_workspace_bytes(0, 5, 1, 1) == 0
+    assert lib.l1b_workspace_bytes(5, 1, 1, 1) == 0
+    # invalid shapes are rejected before any CUDA call
+    assert lib.l1b_prepare(None, 5, 4, None, 0, None) == _lib.L1B_EINVAL
+    lam = (ctypes.c_double * 1)(-1.0)
+    assert lib.l1b_fit_pivots(1, 5, 4, lam, 1, 0, 1, 4, None, 1, 1, 1, 1, 1 << 30, None) == _lib.L1B_EINVAL
+    lam[0] = 1.0
+    assert lib.l1b_fit_pivots(1, 5, 4, lam, 1, 3, 1, 2, None, 1, 1, 1, 1, 1 << 30, None) == _lib.L1B_EINVAL
+
+
+def test_abi_sass_is_sm100a():
+    import subprocess
+    so = _lib.LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
