@@ -12,7 +12,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libl1b200.so")
+LIB_PATH = os.environ.get("L1B200_LIB") or os.path.join(_HERE, "csrc", "libl1b200.so")
 
 # Every symbol include/l1b200.h declares (tests check the export list).
 ABI_SYMBOLS = (

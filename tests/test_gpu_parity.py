@@ -189,13 +189,13 @@ def test_adversarial_ties_vs_oracle(kind):
     if kind == "integers":
         X = np.round(rng.uniform(-4, 4, size=(n, m)))
     elif kind == "sparse":
-        X = np.round(rng.uniform(-10, 10, size=(n, m)), 1)
+        X = np.round(rng.uniform(-10, 10, size=(n, m)) * 8) / 8   # dyadic: prefix sums exact
         X[rng.random(X.shape) < 0.7] = 0.0
     elif kind == "signed_zeros":
         X = np.round(rng.uniform(-3, 3, size=(n, m)))
         X[rng.random(X.shape) < 0.4] = -0.0
     elif kind == "duplicate_rows":
-        base = np.round(rng.uniform(-10, 10, size=(40, m)), 2)
+        base = np.round(rng.uniform(-10, 10, size=(40, m)) * 64) / 64
         X = base[rng.integers(0, 40, size=n)]
     else:  # rank one: every ratio of a column identical up to rounding
         X = np.outer(rng.uniform(-100, 100, size=n), rng.uniform(-1, 1, size=m))

@@ -1,0 +1,34 @@
+"""One prepare + one fit_pivots on a BASELINE config, for ncu launch lists / captures.
+
+    python tools/profile_fit.py [--config c2] [--lam 1.0] [--reps 1]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2402_16712_b200 as l1b  # noqa: E402
+from paper_2402_16712_b200.engine import DeviceFit  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--lam", type=float, default=1.0)
+ap.add_argument("--reps", type=int, default=1)
+a = ap.parse_args()
+shapes = {"c1": (50, 200), "c2": (2000, 2000), "c4": (500, 100000), "c5": (10000, 10000)}
+m, n = shapes[a.config]
+if a.config == "c1":
+    d, _ = l1b.gen_outlier_data(m, n, n // 10, seed=0)
+else:
+    d, _ = l1b.gen_line_data(m, n, seed=0, noise_scale=1.0)
+eng = DeviceFit(np.array(d.values))
+for _ in range(a.reps):
+    eng.prepare()
+    V, E, P, O = eng.fit_pivots([a.lam], want_v=False)
+torch.cuda.synchronize()
+o = O.cpu().numpy()[0]
+print("best pivot", int(np.argmin(o)), float(o.min()))
