@@ -94,6 +94,13 @@ int l1b_absmax(const double* d_X, int64_t n, int64_t m, double* d_out, void* str
  * from IEEE __ddiv_rn into *d_mismatches (device uint64). */
 int l1b_selftest_divide(uint64_t seed, int64_t n_pairs, uint64_t* d_mismatches, void* stream);
 
+/* Diagnostics of the last l1b_fit_pivots on this workspace (no reference
+ * counterpart): h_out[0], h_out[1] = number of (pivot, target) problems the
+ * main selection kernel handed to the exact straggler solver for the last
+ * two penalty weights (even / odd index).  Synchronises the stream. */
+int l1b_fit_stats(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes,
+                  uint64_t* h_out, void* stream);
+
 /* Cumulative count of kernels this library has enqueued in the process
  * (benchmark evidence for "gpu_launches"; no reference counterpart). */
 uint64_t l1b_kernel_launches(void);

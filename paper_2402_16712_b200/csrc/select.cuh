@@ -17,33 +17,34 @@
 // k_select (one thread = one problem, warp = one pivot x 32 targets, CTA = 8
 // pivots sharing every TMA-staged tile of X) runs a fixed pass schedule:
 //   sample   32 strided rows, float ratios sorted in registers -> bracket
-//   pass A   FP32: r ~ a32*y32, 32-bin value-space histogram over the bracket
-//   pass A2  FP32: 32 sub-bins inside A's crossing bin -> window (~1 element)
-//   pass B   exact weights: float classification with a guard band, exact
-//            fl(a/b) only near the window; exact weight below the window,
-//            exact Wneg (signs are exact) -> G; window rows collected and
-//            resolved from exact keys
-//   pass E   residual sum_i |x_ij - v_j x_ip| in row order
-// A problem whose window misses the crossing or holds more than kCapB rows
+//   F passes (P.nfloat of them: 1 for n <= 4096, 2 or 3 beyond): FP32 ratio
+//            r ~ a32*y32 into a 64-slot per-thread histogram (below / 62 bins
+//            / above) of the current range; the crossing bin becomes the
+//            next range, and after the last pass the window [Lw, Hw)
+//   pass B   exact: float classification with a guard band, exact fl(a/b)
+//            only near the window; exact weight below the window, exact
+//            Wneg (signs are exact) -> G; window rows collected (<= CAP).
+//            The column residual is fused in (see the pass for the identity)
+//   resolve  exact keys of the window rows, stable insertion by key, prefix
+//            walk to the crossing, residual of the window rows.
+// A problem whose window misses the crossing or holds more than CAP rows
 // (heavy ties) is queued, with the exact key interval known to hold its
 // crossing, for k_straggle (warp per problem, exact throughout).  The float
 // passes only steer the search: every decision that reaches an output is
 // made with exact integer weights (integer-valued doubles < 2^53, exact in
 // any summation order) and exact f64 keys.
 
-constexpr int kNBA = 32;           // pass-A / A2 bins
-constexpr int kCapB = 8;           // rows collected per problem in pass B
+constexpr int kNB = 64;            // F-pass histogram slots: 0 below, 1..62, 63 above
+constexpr int kNI = kNB - 2;       // interior bins
 constexpr int kDelta = 6;          // +- sample ranks around the estimated crossing
-constexpr int kStages = 3;         // TMA pipeline depth
 constexpr float kGuard = 0x1p-19f; // relative guard band of the float ratios
+constexpr double kBig = 1.7976931348623157e308;  // DBL_MAX: open window side
 
 struct SelParams {
   const double* Xt;      // X in 32-column tiles: ((j/32)*np + i)*32 + j%32
   const float* Xft;      // float copy of Xt
-  const double* gpb;     // shard pivot planes in 8-pivot groups: (g*np + i)*8 + w
-  const double* gpy;
-  const double* gpw;
-  const float2* gpf;
+  const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
+  const float2* gpf;     // shard (float y_ip, float |x_ip|) in 8-pivot groups
   const double* Xc;      // column-major m x n
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
@@ -56,12 +57,20 @@ struct SelParams {
   int64_t n, m, mp, np;   // np: plane row length (multiple of 32)
   int64_t p_begin, p_stride, npiv;
   double lam;
+  int nfloat;            // number of F passes (1..3)
   double* V;             // [npiv][m]
   double* E;             // [npiv][m]
   Straggler* strag;
   unsigned long long* nstrag;
   int* status;
 };
+
+// acc += x if p, exactly (x, acc integer-valued): one select of the high
+// word of 1.0 and one DFMA, instead of the add-and-select-both-halves the
+// compiler's if-conversion emits.
+__device__ __forceinline__ void padd(double& acc, double x, bool p) {
+  acc = __fma_rn(x, __hiloint2double(p ? 0x3ff00000 : 0, 0), acc);
+}
 
 // Exact region test: returns false for a dead column, else sets G.  All
 // operands are integers below 2^53 held in doubles, so every step is exact
@@ -79,42 +88,44 @@ __device__ __forceinline__ bool region_G(double Tq, double wneg, double Lsc, dou
 }
 
 // smem planes of one staged chunk (kRows rows); a pass stages only the
-// planes it reads, so its stage is small and the 60 KB ring holds many.
-constexpr int kTileF = kRows * 32 * 4;           // a32
-constexpr int kTileA = kRows * 32 * 8;           // a (f64)
-constexpr int kPlane8 = kWarps * kRows * 8;      // pf / pb / py / pw: [row][8 pivots]
-constexpr int kRing = 60 * 1024;
-constexpr int kMaxStages = 10;
-constexpr int kHist = kNBA + 2;   // per-thread histogram slots (A2: below / 32 / above)
+// planes it reads.  Shared-memory wavefronts, not arithmetic, bound this
+// kernel, so every staged byte is one a pass actually uses.
+constexpr int kTileF = kRows * 32 * 4;           // a32 tile [row][32 targets]
+constexpr int kTileA = kRows * 32 * 8;           // a (f64) tile
+constexpr int kPlaneF = kWarps * kRows * 8;      // (y32, w32) [row][8 pivots]
+constexpr int kPlaneBW = kWarps * kRows * 16;    // (x_ip, wq) [row][8 pivots]
+constexpr int kRingF = 32 * 1024;                // ring of the F passes
+constexpr int kHistBytes = kNB * kBS * 4;        // per-thread histograms [slot][thread]
+constexpr int kRingB = kRingF + kHistBytes;      // pass B also streams through the histogram space
+constexpr int kMaxStages = 8;
 
-template <typename RowT>
+template <typename RowT, int CAP>
 constexpr size_t select_smem() {
-  return (size_t)kRing + sizeof(float) * kHist * kBS + sizeof(RowT) * kCapB * kBS;
+  return (size_t)kRingB + sizeof(RowT) * CAP * kBS;
 }
 
-enum : unsigned { W_F = 1, W_A = 2, W_PF = 4, W_PB = 8, W_PY = 16, W_PW = 32 };
+enum : unsigned { W_F = 1, W_A = 2, W_PF = 4, W_BW = 8 };
 
 // Byte offsets of the planes inside one stage for a given plane set.
 struct StageLayout {
-  int f, a, pf, pb, py, pw, bytes, nst;
-  __device__ explicit StageLayout(unsigned want) {
+  int f, a, pf, bw, bytes, nst;
+  __device__ StageLayout(unsigned want, int ring) {
     int o = 0;
     f = o; o += (want & W_F) ? kTileF : 0;
     a = o; o += (want & W_A) ? kTileA : 0;
-    pf = o; o += (want & W_PF) ? kPlane8 : 0;
-    pb = o; o += (want & W_PB) ? kPlane8 : 0;
-    py = o; o += (want & W_PY) ? kPlane8 : 0;
-    pw = o; o += (want & W_PW) ? kPlane8 : 0;
+    pf = o; o += (want & W_PF) ? kPlaneF : 0;
+    bw = o; o += (want & W_BW) ? kPlaneBW : 0;
     bytes = o;
-    nst = min(kMaxStages, kRing / o);
+    nst = min(kMaxStages, ring / o);
   }
 };
 
-template <typename RowT>
+template <typename RowT, int CAP>
 __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
+  static_assert(CAP * 8 <= kNB * 4, "resolve keys live in the histogram space");
   extern __shared__ __align__(128) unsigned char smem[];
-  float* hist = (float*)(smem + kRing);                                   // [kHist][kBS]
-  RowT* cbuf = (RowT*)(hist + kHist * kBS);                              // [kCapB][kBS]
+  float* hist = (float*)(smem + kRingF);                                  // [kNB][kBS]
+  RowT* cbuf = (RowT*)(smem + kRingB);                                    // [CAP][kBS]
   __shared__ __align__(8) unsigned long long full[kMaxStages], empty[kMaxStages];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -130,11 +141,14 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
 
   double Tq = 0.0;
   double Lsc = 0.0;
+  int sp = 0;
   if (piv_ok && !degenerate) {
     Tq = P.tq[p];
-    Lsc = ldexp(P.lam, P.spow[p]);
+    sp = P.spow[p];
+    Lsc = ldexp(P.lam, sp);
   }
-  const float lam32 = (float)P.lam;
+  const double unit = ldexp(1.0, -sp);
+  const bool exact_f = P.nfloat >= 2;  // multi-pass: exact bases and exact Wneg in the F passes
 
   // ---- TMA pipeline ----------------------------------------------------------
   // Producer: the lanes of warp 0 issue the bulk copies of chunk c into stage
@@ -151,8 +165,6 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   }
   __syncthreads();
   unsigned fphase = 0, ephase = 0, used = 0;  // per-barrier bits
-  int nvalid = 0;
-  for (int w = 0; w < kWarps; ++w) nvalid += ((int64_t)blockIdx.y * kWarps + w) < P.npiv;
   const int64_t nch = (n + kRows - 1) / kRows;
   const int64_t tbase = (int64_t)blockIdx.x * np * 32;  // this CTA's target tile
   const int64_t gbase = (int64_t)blockIdx.y * np * 8;   // this CTA's pivot group
@@ -171,17 +183,16 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       mbar_expect_tx(&full[st], (unsigned)L.bytes);
       if (want & W_F) bulk_g2s(base + L.f, P.Xft + tbase + i0 * 32, kTileF, &full[st]);
       if (want & W_A) bulk_g2s(base + L.a, P.Xt + tbase + i0 * 32, kTileA, &full[st]);
-      if (want & W_PF) bulk_g2s(base + L.pf, P.gpf + gbase + i0 * 8, kPlane8, &full[st]);
-      if (want & W_PB) bulk_g2s(base + L.pb, P.gpb + gbase + i0 * 8, kPlane8, &full[st]);
-      if (want & W_PY) bulk_g2s(base + L.py, P.gpy + gbase + i0 * 8, kPlane8, &full[st]);
-      if (want & W_PW) bulk_g2s(base + L.pw, P.gpw + gbase + i0 * 8, kPlane8, &full[st]);
+      if (want & W_PF) bulk_g2s(base + L.pf, P.gpf + gbase + i0 * 8, kPlaneF, &full[st]);
+      if (want & W_BW) bulk_g2s(base + L.bw, P.gbw + gbase + i0 * 8, kPlaneBW, &full[st]);
     }
     __syncwarp();
   };
   // body(stage base, layout, rows, first_row) on every chunk
-  auto sweep = [&](unsigned want, bool busy, auto&& body) {
-    const StageLayout L(want);
-    __syncthreads();  // every stage of the previous pass has been consumed
+  auto sweep = [&](unsigned want, int ring, bool busy, auto&& body) {
+    const StageLayout L(want, ring);
+    fence_proxy_async();  // generic writes to the ring space (histograms) before async copies
+    __syncthreads();      // every stage of the previous pass has been consumed
     for (int64_t c = 0; c < min((int64_t)(L.nst - 1), nch); ++c) issue(L, c, want);
     for (int64_t c = 0; c < nch; ++c) {
       if (c + L.nst - 1 < nch) issue(L, c + L.nst - 1, want);
@@ -198,9 +209,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   auto tA = [&](const unsigned char* b, const StageLayout& L) { return (const double*)(b + L.a); };
   // plane entries of row r for this warp's pivot: [r * 8 + warp]
   auto pF = [&](const unsigned char* b, const StageLayout& L) { return (const float2*)(b + L.pf) + warp; };
-  auto pB = [&](const unsigned char* b, const StageLayout& L) { return (const double*)(b + L.pb) + warp; };
-  auto pY = [&](const unsigned char* b, const StageLayout& L) { return (const double*)(b + L.py) + warp; };
-  auto pW = [&](const unsigned char* b, const StageLayout& L) { return (const double*)(b + L.pw) + warp; };
+  auto pBW = [&](const unsigned char* b, const StageLayout& L) { return (const double2*)(b + L.bw) + warp; };
 
   // ---- sample: float ratios of 32 strided rows, sorted -> value bracket ----
   float lo = 0.f, hi = 0.f;
@@ -261,185 +270,274 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     lo -= e;
     hi += e;
   }
-  const bool warp_active = __any_sync(0xffffffffu, active);
 
-  // ---- pass A: 32-bin FP32 histogram over [lo, hi) (edge bins = tails) ------
-  // bin(r) = RN(clamp(r * s + o)) is monotone in r: interior bin b <-> r in
-  // [lo + (b-1) w, lo + b w), w = (hi - lo) / 30.
-  const float sA = (float)(kNBA - 2) / (hi - lo);
-  const float oA = 0.5f - lo * sA;
+  // ---- F passes: 64-slot FP32 histograms, each narrowing the range ---------
+  // slot(r) = RN(63 * sat(r * A + B)): slot 0 <-> r < lo, slot b in 1..62 <->
+  // r in [lo + (b-1) w, lo + b w) with w = (hi - lo) / 62, slot 63 <-> r >= hi
+  // (up to float rounding at the edges, which the margins absorb).  The
+  // slot address is one integer multiply-add of the magic-rounded bits.
+  // Single pass (n <= 4096): float sums throughout -- a bin holds ~1/100 of
+  // the weight, far above float rounding.  Several passes (large n): the bins
+  // of later passes are tiny, so every pass also sums the exact weight of its
+  // slot 0 (where the walk to the crossing starts) and pass 1 the exact Wneg
+  // (exact G, and dead columns drop out of the later passes).
+  double wneg = 0.0, G = 0.0;
+  bool live = active;
+  double Lw = -kBig, Hw = kBig;   // final window [Lw, Hw)
+  float G32 = 0.f;
+  for (int pass = 0; pass < P.nfloat; ++pass) {
+    const float A = (62.f / 63.f) / (hi - lo);
+    const float B = 0.5f / 63.f - lo * A;
 #pragma unroll
-  for (int b = 0; b < kNBA; ++b) hist[b * kBS + tid] = 0.f;
-  float wn32 = 0.f;
-  sweep(W_F | W_PF, warp_active, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-    const float* ta = tF(sb, L);
-    const float2* pf = pF(sb, L);
+    for (int b = 0; b < kNB; ++b) hist[b * kBS + tid] = 0.f;
+    const unsigned hbase = smem_u32(hist + tid) - 0x4B000000u * (unsigned)(kBS * 4);
+    const bool busy = __any_sync(0xffffffffu, live);
+    // the histogram update shared by every variant; returns the slot bits
+    auto bin = [&](float q, float wgt) {
+      const float u = __saturatef(fmaf(q, A, B));
+      const unsigned bits = __float_as_uint(fmaf(u, 63.f, 8388608.f));
+      const unsigned addr = hbase + bits * (unsigned)(kBS * 4);
+      float h;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h) : "r"(addr));
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(h + wgt));
+      return bits;
+    };
+    double base;
+    if (!exact_f) {  // single float pass (pass == 0)
+      float wn32 = 0.f;
+      sweep(W_F | W_PF, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
+        const float* ta = tF(sb, L);
+        const float2* pf = pF(sb, L);
 #pragma unroll 4
-    for (int r = 0; r < rmax; ++r) {
-      const float2 yw = pf[r * 8];
-      const float q = ta[r * 32 + lane] * yw.x;
-      const float t = fminf(fmaxf(fmaf(q, sA, oA), 0.f), (float)(kNBA - 1));
-      const int b = __float_as_int(t + 8388608.f) - 0x4B000000;
-      hist[b * kBS + tid] += yw.y;
-      if (q < 0.f) wn32 += yw.y;
-    }
-  });
-  float T32 = 0.f;
+        for (int r = 0; r < rmax; ++r) {
+          const float2 yw = pf[r * 8];
+          const float q = ta[r * 32 + lane] * yw.x;
+          bin(q, yw.y);
+          if (q < 0.f) wn32 += yw.y;
+        }
+      });
+      float T32 = 0.f;
 #pragma unroll
-  for (int b = 0; b < kNBA; ++b) T32 += hist[b * kBS + tid];
-  const float D32 = T32 - 2.f * wn32;
-  const float G32 = 0.5f * (T32 - (D32 < -lam32 ? -lam32 : (D32 >= lam32 ? lam32 : 0.f)));
-  // A2 range: the crossing bin of A (edge bins: a widened band beyond the bracket)
-  float lo2, hi2;
-  {
-    float cum = 0.f;
-    int bw = kNBA - 1;
-    bool got = false;
-#pragma unroll
-    for (int b = 0; b < kNBA; ++b) {
-      float h = hist[b * kBS + tid];
-      if (!got && cum + h > G32) { bw = b; got = true; }
-      if (!got) cum += h;
+      for (int b = 0; b < kNB; ++b) T32 += hist[b * kBS + tid];
+      const float lam32 = (float)P.lam;
+      const float D32 = T32 - 2.f * wn32;
+      G32 = 0.5f * (T32 - (D32 < -lam32 ? -lam32 : (D32 >= lam32 ? lam32 : 0.f)));
+      // certainly dead (float error of D32 is far below the slack): skip pass B
+      if (fabsf(D32) + 1e-7f * (float)n * T32 < lam32 * (1.f - 1e-6f)) live = false;
+      base = (double)hist[tid];
+    } else if (pass == 0) {
+      double wlow = 0.0;
+      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
+        const float* ta = tF(sb, L);
+        const float2* pf = pF(sb, L);
+        const double2* bw = pBW(sb, L);
+#pragma unroll 4
+        for (int r = 0; r < rmax; ++r) {
+          const float2 yw = pf[r * 8];
+          const float q = ta[r * 32 + lane] * yw.x;
+          const unsigned bits = bin(q, yw.y);
+          const double wq = bw[r * 8].y;
+          padd(wneg, wq, q < 0.f);                 // exact: signs of q32 are exact
+          padd(wlow, wq, bits == 0x4B000000u);     // exact weight of slot 0
+        }
+      });
+      if (live && !region_G(Tq, wneg, Lsc, &G)) live = false;  // dead column
+      base = wlow * unit;
+    } else {
+      double wlow = 0.0;
+      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
+        const float* ta = tF(sb, L);
+        const float2* pf = pF(sb, L);
+        const double2* bw = pBW(sb, L);
+#pragma unroll 4
+        for (int r = 0; r < rmax; ++r) {
+          const float2 yw = pf[r * 8];
+          const float q = ta[r * 32 + lane] * yw.x;
+          padd(wlow, bw[r * 8].y, bin(q, yw.y) == 0x4B000000u);  // exact weight below the range
+        }
+      });
+      base = wlow * unit;
     }
-    const float w = (hi - lo) / (float)(kNBA - 2);
-    if (bw == 0) { lo2 = lo - 8.f * (hi - lo); hi2 = lo + 0.5f * w; }
-    else if (bw == kNBA - 1) { lo2 = hi - 0.5f * w; hi2 = hi + 8.f * (hi - lo); }
-    else { lo2 = lo + ((float)bw - 1.5f) * w; hi2 = lo + ((float)bw + 0.5f) * w; }
+    // crossing slot: walk the interior bins from the weight below the range
+    const double Gd = exact_f ? G * unit : (double)G32;
+    double cum = base;
+    int bw = 0;
+    if (!(cum > Gd)) {
+      bw = kNB - 1;
+#pragma unroll 8
+      for (int b = 1; b < kNB - 1; ++b) {
+        const double h = (double)hist[b * kBS + tid];
+        if (cum + h > Gd) { bw = b; break; }
+        cum += h;
+      }
+    }
+    const float w = (hi - lo) / (float)kNI;
+    if (pass + 1 < P.nfloat) {
+      float nlo, nhi;
+      if (bw == 0) { nlo = lo - 8.f * (hi - lo); nhi = lo + 0.05f * w; }
+      else if (bw == kNB - 1) { nlo = hi - 0.05f * w; nhi = hi + 8.f * (hi - lo); }
+      else { nlo = lo + ((float)bw - 1.05f) * w; nhi = lo + ((float)bw + 0.05f) * w; }
+      lo = nlo;
+      hi = nhi;
+      if (!(hi > lo)) {
+        float e = fmaxf(fabsf(lo), 1e-30f) * 1e-3f;
+        lo -= e;
+        hi += e;
+      }
+    } else {
+      const double wd = ((double)hi - (double)lo) / (double)kNI;
+      if (bw == 0) {
+        Hw = (double)lo + (fabs((double)lo) * 0x1p-18 + wd * 0.02);
+      } else if (bw == kNB - 1) {
+        Lw = (double)hi - (fabs((double)hi) * 0x1p-18 + wd * 0.02);
+      } else {
+        const double a = (double)lo + (double)(bw - 1) * wd, b = a + wd;
+        Lw = a - (fabs(a) * 0x1p-18 + wd * 0.02);
+        Hw = b + (fabs(b) * 0x1p-18 + wd * 0.02);
+      }
+    }
   }
 
-  // ---- pass A2: 32 sub-bins over [lo2, hi2); slot 0 = below, 33 = above ----
-  const float sA2 = (float)kNBA / (hi2 - lo2);
-  const float oA2 = 0.5f - lo2 * sA2;
-#pragma unroll
-  for (int b = 0; b < kHist; ++b) hist[b * kBS + tid] = 0.f;
-  sweep(W_F | W_PF, warp_active, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-    const float* ta = tF(sb, L);
-    const float2* pf = pF(sb, L);
-#pragma unroll 4
-    for (int r = 0; r < rmax; ++r) {
-      const float2 yw = pf[r * 8];
-      const float q = ta[r * 32 + lane] * yw.x;
-      const float t = fminf(fmaxf(fmaf(q, sA2, oA2), 0.f), (float)(kHist - 1));
-      hist[(__float_as_int(t + 8388608.f) - 0x4B000000) * kBS + tid] += yw.y;
-    }
-  });
-  // window = the crossing sub-bin, widened by the float error band
-  double Lw = -INFINITY, Hw = INFINITY;
-  {
-    float cum = hist[tid];  // slot 0: below lo2
-    int bw = -1;
-#pragma unroll
-    for (int b = 0; b < kNBA; ++b) {
-      float h = hist[(b + 1) * kBS + tid];
-      if (bw < 0 && cum + h > G32) bw = b;
-      if (bw < 0) cum += h;
-    }
-    const double w2 = ((double)hi2 - (double)lo2) / (double)kNBA;
-    if (bw >= 0) {
-      double a = (double)lo2 + (double)bw * w2, b = a + w2;
-      Lw = a - (fabs(a) * 0x1p-18 + w2 * 0.02);
-      Hw = b + (fabs(b) * 0x1p-18 + w2 * 0.02);
-    } else if (cum <= G32) {  // beyond hi2: leave the window open upward
-      Lw = (double)hi2 - fabs((double)hi2) * 0x1p-18;
-    } else {                  // below lo2
-      Hw = (double)lo2 + fabs((double)lo2) * 0x1p-18;
-    }
-  }
-
-  // ---- pass B: exact weights; exact ratios only near the window ------------
-  // Float ratios carry < 2^-21 relative error, so any element whose float
-  // ratio is outside [Lw, Hw) by more than the guard band is classified
-  // exactly without dividing.  Signs are exact (FLOATSAFE inputs).
+  // ---- pass B: exact weights + fused residual; the window is collected -----
+  // Float ratios carry < 2^-21 relative error, so an element whose float
+  // ratio is below Lg (Lw less a guard band) is certainly below the window
+  // and one at or above Hg certainly above it (signs are exact: FLOATSAFE
+  // inputs).  Everything in [Lg, Hg) -- the window and its guard bands -- is
+  // only collected (row index) and classified exactly in the resolve, so the
+  // pass is branch-free.
+  // Residual: with one finite reference point c0 in {Lw, Hw} and v in
+  // [Lw, Hw), every element outside the window satisfies
+  //   |x_ij - v x_ip| = |x_ij - c0 x_ip| +- (v - c0) |x_ip|   (+ below, - above)
+  // exactly in real arithmetic, so the pass sums |x_ij - c0 x_ip| now and the
+  // resolve adds (v - c0)(W_below - W_above); (v - c0) is window-sized, so
+  // nothing cancels.  Dropped rows (x_ip = 0: y32 = 0, wq = 0, exact ratio
+  // NaN) carry no weight and add |x_ij|.
   const float Lg = (float)(Lw - fabs(Lw) * (double)kGuard);
   const float Hg = (float)(Hw + fabs(Hw) * (double)kGuard);
-  double wb = 0.0, win = 0.0, wneg = 0.0;
+  const double c0 = Lw > -kBig ? Lw : Hw;
+  double wb = 0.0, es = 0.0;
   int cnt = 0;
-  sweep(W_F | W_PF | W_PW | W_A | W_PB | W_PY, warp_active,
-        [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
+  const unsigned cb0 = smem_u32(cbuf + tid);
+  auto bbody = [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0, auto want_wneg) {
     const float* ta = tF(sb, L);
     const float2* pf = pF(sb, L);
-    const double* pw = pW(sb, L);
+    const double2* bwp = pBW(sb, L);
+    const double* xa = tA(sb, L);
 #pragma unroll 4
     for (int r = 0; r < rmax; ++r) {
       const float q32 = ta[r * 32 + lane] * pf[r * 8].x;
-      const double wq = pw[r * 8];
-      if (q32 < 0.f) wneg += wq;
-      if (q32 < Lg) wb += wq;
-      if (q32 >= Lg && q32 < Hg) {  // near or inside: decide exactly
-        const double q = ratio_fast(tA(sb, L)[r * 32 + lane], pB(sb, L)[r * 8], pY(sb, L)[r * 8]);
-        if (q < Lw) {
-          wb += wq;
-        } else if (q < Hw) {
-          win += wq;
-          if (cnt < kCapB) cbuf[cnt * kBS + tid] = (RowT)(i0 + r);
-          ++cnt;
-        }
+      const double2 bw = bwp[r * 8];  // (x_ip, wq)
+      const double a = xa[r * 32 + lane];
+      if (decltype(want_wneg)::value) padd(wneg, bw.y, q32 < 0.f);
+      const bool below = q32 < Lg;
+      const bool inw = !below && q32 < Hg;
+      padd(wb, bw.y, below);
+      if (inw && cnt < CAP) {
+        const unsigned addr = cb0 + (unsigned)(cnt * kBS * sizeof(RowT));
+        const RowT row = (RowT)(i0 + r);
+        if (sizeof(RowT) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)row));
+        else asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"((unsigned)row));
       }
+      cnt += inw;
+      es += fabs(__fma_rn(-bw.x, c0, a));  // the resolve takes the window rows back out
     }
-  });
+  };
+  const bool busyB = __any_sync(0xffffffffu, live);
+  if (exact_f)
+    sweep(W_F | W_A | W_PF | W_BW, kRingB, busyB, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
+      bbody(sb, L, rmax, i0, std::false_type{});
+    });
+  else
+    sweep(W_F | W_A | W_PF | W_BW, kRingB, busyB, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
+      bbody(sb, L, rmax, i0, std::true_type{});
+    });
+  __syncthreads();  // the ring (incl. the histogram space) is free for the resolve keys
 
-  double v = 0.0;
+  if (live && !exact_f && !region_G(Tq, wneg, Lsc, &G)) live = false;  // exact dead test
+  double v = 0.0, e = 0.0;
   bool done = !active;
+  unsigned long long slo = 0, shi = ~0ULL;  // straggler interval
   if (active) {
-    double G = 0.0;
-    if (!region_G(Tq, wneg, Lsc, &G)) {
-      done = true;  // dead column (fit.py:60-63 returns +0.0)
-    } else if (wb <= G && G < wb + win && cnt <= kCapB) {
-      // resolve: exact keys of the window rows into this thread's (now free)
-      // histogram slots, stable insertion by key, then the prefix walk
-      unsigned long long* key = (unsigned long long*)hist;       // [kCapB][kBS]
-      double* wgt = (double*)hist + kCapB * kBS;                 // [kCapB][kBS]
+    if (!live) {
+      done = true;  // dead column (fit.py:60-63 returns +0.0): residual = sum_i |x_ij|
+      e = P.colsum[j];
+    } else if (cnt <= CAP) {
+      // resolve: exact keys of the collected rows; guard-band rows below Lw /
+      // at or above Hw join the sides, the rest (the window) is sorted by
+      // (key, row) -- stable insertion, rows were collected in ascending
+      // order -- and walked to the crossing
+      unsigned long long* key = (unsigned long long*)hist;  // [CAP][kBS]
       const double* xcol = P.Xc + jc * n;
+      const double* pbp = P.pb + p * P.np;
+      const double* pyp = P.py + p * P.np;
+      const double* pwp = P.pw + p * P.np;
+      const unsigned long long KL = key64(Lw), KH = key64(Hw);
+      int nw = 0;
+      double win = 0.0;
       for (int c = 0; c < cnt; ++c) {
         const int row = (int)cbuf[c * kBS + tid];
-        const unsigned long long k = key64(ratio_fast(xcol[row], P.pb[p * P.np + row], P.py[p * P.np + row]));
-        const double w = P.pw[p * P.np + row];
-        int d = c;
-        while (d > 0 && key[(d - 1) * kBS + tid] > k) {
-          key[d * kBS + tid] = key[(d - 1) * kBS + tid];
-          wgt[d * kBS + tid] = wgt[(d - 1) * kBS + tid];
-          cbuf[d * kBS + tid] = cbuf[(d - 1) * kBS + tid];
-          --d;
+        const double a = xcol[row], b = pbp[row], y = pyp[row], w = pwp[row];
+        const double q = ratio_fast(a, b, y);
+        const unsigned long long k = key64(q);
+        if (w == 0.0 || k < KL || k >= KH) {  // dropped row, or a guard-band row outside the window
+          if (w != 0.0 && k < KL) wb += w;
+        } else {
+          es -= fabs(__fma_rn(-b, c0, a));  // pass B added every row
+          win += w;
+          int d = nw++;
+          while (d > 0 && key[(d - 1) * kBS + tid] > k) {
+            key[d * kBS + tid] = key[(d - 1) * kBS + tid];
+            cbuf[d * kBS + tid] = cbuf[(d - 1) * kBS + tid];
+            --d;
+          }
+          key[d * kBS + tid] = k;
+          cbuf[d * kBS + tid] = (RowT)row;
         }
-        key[d * kBS + tid] = k;
-        wgt[d * kBS + tid] = w;
-        cbuf[d * kBS + tid] = (RowT)row;
       }
-      double cum = wb;
-      for (int c = 0; c < cnt && !done; ++c) {
-        cum += wgt[c * kBS + tid];
-        if (cum > G) {
-          const unsigned long long k = key[c * kBS + tid];
+      if (wb <= G && G < wb + win) {
+        double cum = wb;
+        for (int c = 0; c < nw && !done; ++c) {
           const int row = (int)cbuf[c * kBS + tid];
-          v = k == kZeroKey ? __ddiv_rn(xcol[row], P.pb[p * P.np + row]) : key64_inv(k);
-          done = true;
+          cum += pwp[row];
+          if (cum > G) {
+            const unsigned long long k = key[c * kBS + tid];
+            v = k == kZeroKey ? __ddiv_rn(xcol[row], pbp[row]) : key64_inv(k);
+            done = true;
+          }
         }
+        double ew = 0.0;
+        for (int c = 0; c < nw; ++c) {
+          const int row = (int)cbuf[c * kBS + tid];
+          ew += fabs(__dsub_rn(xcol[row], __dmul_rn(pbp[row], v)));  // core.py:93 rounding
+        }
+        const double wa = Tq - wb - win;  // exact
+        e = es + ew + (v - c0) * ((wb - wa) * unit);
+      } else if (G < wb) {  // exact weights put the crossing below / above the window
+        slo = 0;
+        shi = KL - 1;
+      } else {
+        slo = KH;
+        shi = ~0ULL;
       }
+    } else {
+      // window overflow (heavy ties / wide window): the crossing is most
+      // likely in [Lg, Hg); the straggler solver widens the interval itself
+      // if it is not
+      slo = key64((double)Lg - fabs((double)Lg) * 0x1p-20);
+      shi = key64((double)Hg + fabs((double)Hg) * 0x1p-20);
     }
     if (!done) {
       Straggler s;
       s.kk = (int)kk;
       s.j = (int)j;
       s.G = G;
-      const unsigned long long KL = Lw == -INFINITY ? 0ULL : key64(Lw);
-      const unsigned long long KH = Hw == INFINITY ? ~0ULL : key64(Hw);
-      if (G < wb) { s.lo = 0; s.hi = KL - 1; s.wb = 0; }
-      else if (G >= wb + win) { s.lo = KH; s.hi = ~0ULL; s.wb = wb + win; }
-      else { s.lo = KL; s.hi = KH - 1; s.wb = wb; }
+      s.lo = slo;
+      s.hi = shi;
+      s.wb = 0.0;
       unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
       P.strag[slot] = s;
     }
   }
-
-  // ---- pass E: residual in row order ---------------------------------------
-  double e = 0.0;
-  const bool warp_err = __any_sync(0xffffffffu, active && done);
-  sweep(W_A | W_PB, warp_err, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-    const double* ta = tA(sb, L);
-    const double* pb = pB(sb, L);
-#pragma unroll 4
-    for (int r = 0; r < rmax; ++r) e += fabs(__dsub_rn(ta[r * 32 + lane], __dmul_rn(pb[r * 8], v)));
-  });
 
   if (piv_ok && j < m) {
     if (degenerate) {
@@ -494,9 +592,10 @@ __global__ void k_queue_all(SelParams P) {
 // narrows to the crossing bucket.  Ratios use the hoisted division when
 // SAFE, IEEE __ddiv_rn otherwise.
 
-constexpr int kSWarps = 4;
-constexpr int kSCap = 1024;
-constexpr int kSBins = 256;
+constexpr int kSWarps = 8;
+constexpr int kSCap = 256;   // interval elements collected and sorted per round
+constexpr int kSBins = 256;  // radix bins when the interval holds more
+constexpr int kSUnroll = 4;  // rows per lane in flight (loads hoisted for ILP)
 
 struct SEnt {
   unsigned long long k;
@@ -505,12 +604,12 @@ struct SEnt {
   int pad;
 };
 
-constexpr size_t kStraggleSmem = (size_t)kSWarps * (kSCap * sizeof(SEnt) + kSBins * sizeof(double));
+constexpr size_t kStraggleSmem =
+    (size_t)kSWarps * (kSCap * sizeof(SEnt) + kSBins * sizeof(unsigned long long));
 
 template <bool SAFE>
-__device__ __forceinline__ double sratio(const SelParams& P, int64_t p, int64_t i, int64_t j) {
-  const double a = P.Xc[j * P.n + i], b = P.pb[p * P.np + i];
-  if (SAFE) return ratio_fast(a, b, P.py[p * P.np + i]);
+__device__ __forceinline__ double sratio(const SelParams& P, double a, double b, double y) {
+  if (SAFE) return ratio_fast(a, b, y);
   return b != 0.0 ? __ddiv_rn(a, b) : __longlong_as_double(0x7ff8000000000000LL);
 }
 
@@ -519,11 +618,43 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// Visit every row with nonzero weight of problem (p, j): f(row, key, weight).
+// kSUnroll rows per lane are loaded before any is used, so a warp keeps
+// 4 x 4 independent loads in flight per lane (the loop is latency-bound).
+template <bool SAFE, typename F>
+__device__ __forceinline__ void for_rows(const SelParams& P, int64_t p, int64_t j, int lane, F&& f) {
+  const int64_t n = P.n;
+  const double* xc = P.Xc + j * n;
+  const double* pb = P.pb + p * P.np;
+  const double* py = P.py + p * P.np;
+  const double* pw = P.pw + p * P.np;
+  for (int64_t i0 = 0; i0 < n; i0 += 32 * kSUnroll) {
+    double a[kSUnroll], b[kSUnroll], y[kSUnroll], w[kSUnroll];
+#pragma unroll
+    for (int u = 0; u < kSUnroll; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      const bool ok = i < n;
+      a[u] = ok ? xc[i] : 0.0;
+      b[u] = ok ? pb[i] : 0.0;
+      y[u] = ok ? py[i] : 0.0;
+      w[u] = ok ? pw[i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kSUnroll; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      const bool ok = i < n && w[u] != 0.0;
+      const unsigned long long k = ok ? key64(sratio<SAFE>(P, a[u], b[u], y[u])) : 0ULL;
+      f(ok, (int)i, k, w[u]);
+    }
+  }
+}
+
 template <bool SAFE>
 __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
   extern __shared__ __align__(16) unsigned char ssm[];
   SEnt(*ent)[kSCap] = reinterpret_cast<SEnt(*)[kSCap]>(ssm);
-  double(*bins)[kSBins] = reinterpret_cast<double(*)[kSBins]>(ssm + (size_t)kSWarps * kSCap * sizeof(SEnt));
+  unsigned long long(*bins)[kSBins] =
+      reinterpret_cast<unsigned long long(*)[kSBins]>(ssm + (size_t)kSWarps * kSCap * sizeof(SEnt));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned long long total = *P.nstrag;
   const int64_t n = P.n, m = P.m;
@@ -531,24 +662,20 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
        t += (unsigned long long)gridDim.x * kSWarps) {
     Straggler s = P.strag[t];
     const int64_t kk = s.kk, j = s.j, p = P.p_begin + kk * P.p_stride;
-    const double* pwp = P.pw + p * P.np;
     const double Tq = P.tq[p];
     const double Lsc = ldexp(P.lam, P.spow[p]);
-    double G = s.G, wb = s.wb;
+    double G = s.G;
     unsigned long long lo = s.lo, hi = s.hi;
     bool dead = false;
     if (G < 0.0) {  // exact Wneg and key range first
       double wneg = 0.0;
       unsigned long long kmin = ~0ULL, kmax = 0;
-      for (int64_t i = lane; i < n; i += 32) {
-        const double w = pwp[i];
-        if (w == 0.0) continue;
-        const double q = sratio<SAFE>(P, p, i, j);
-        const unsigned long long k = key64(q);
-        if (q < 0.0) wneg += w;
+      for_rows<SAFE>(P, p, j, lane, [&](bool ok, int, unsigned long long k, double w) {
+        if (!ok) return;
+        if (k < kZeroKey) wneg += w;  // key below +-0 <=> ratio < 0
         kmin = min(kmin, k);
         kmax = max(kmax, k);
-      }
+      });
       wneg = warp_sum(wneg);
       for (int o = 16; o; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
@@ -557,30 +684,62 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
       dead = !region_G(Tq, wneg, Lsc, &G);
       lo = kmin;
       hi = kmax;
-      wb = 0.0;
     }
     double v = 0.0;
     bool ok = dead;
-    for (int round = 0; round < 40 && !ok; ++round) {
-      int base = 0;
-      for (int64_t i0 = 0; i0 < n; i0 += 32) {
-        const int64_t i = i0 + lane;
-        bool in = false;
-        unsigned long long k = 0;
-        double w = 0.0;
-        if (i < n) {
-          w = pwp[i];
-          if (w != 0.0) {
-            k = key64(sratio<SAFE>(P, p, i, j));
-            in = k >= lo && k <= hi;
-          }
+    // Each round visits every row once, recomputing the exact weight below
+    // the interval (so an interval from k_select need not come with one),
+    // and either collects the interval (<= kSCap elements: sort + walk) or
+    // narrows it by a 256-bin exact radix histogram.  A walk that misses
+    // moves the interval to the side holding the crossing.
+    for (int round = 0; round < 64 && !ok; ++round) {
+      double wbl = 0.0;  // exact weight with key < lo
+      if (lo == hi) {
+        // one key left (heavy exact ties): the value is that key; only a
+        // zero needs the crossing row itself (its sign), found by an
+        // in-order prefix walk over the tied rows
+        if (lo != kZeroKey) {
+          v = key64_inv(lo);
+          ok = true;
+          break;
         }
+        for_rows<SAFE>(P, p, j, lane, [&](bool okr, int, unsigned long long k, double w) {
+          if (okr && k < lo) wbl += w;
+        });
+        double cum = warp_sum(wbl);
+        int hit_row = -1;
+        for_rows<SAFE>(P, p, j, lane, [&](bool okr, int row, unsigned long long k, double w) {
+          double x = (okr && k == lo) ? w : 0.0;
+          for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          const unsigned cm = __ballot_sync(0xffffffffu, x > 0.0 && cum + x > G);
+          if (hit_row < 0 && cm) hit_row = __shfl_sync(0xffffffffu, row, __ffs(cm) - 1);
+          cum += __shfl_sync(0xffffffffu, x, 31);
+        });
+        if (hit_row < 0) break;
+        v = __ddiv_rn(P.Xc[j * n + hit_row], P.pb[p * P.np + hit_row]);
+        ok = true;
+        break;
+      }
+      // collect the interval's elements (in row order) if they fit
+      int base = 0;
+      for_rows<SAFE>(P, p, j, lane, [&](bool okr, int row, unsigned long long k, double w) {
+        const bool in = okr && k >= lo && k <= hi;
+        if (okr && k < lo) wbl += w;
         const unsigned mask = __ballot_sync(0xffffffffu, in);
         const int pos = base + __popc(mask & ((1u << lane) - 1));
-        if (in && pos < kSCap) ent[warp][pos] = SEnt{k, w, (int)i, 0};
+        if (in && pos < kSCap) ent[warp][pos] = SEnt{k, w, row, 0};
         base += __popc(mask);
-      }
+      });
+      wbl = warp_sum(wbl);
       __syncwarp();
+      if (G < wbl) {  // the crossing lies below the interval
+        hi = lo - 1;
+        lo = 0;
+        continue;
+      }
       if (base <= kSCap) {
         int np2 = 1;
         while (np2 < base) np2 <<= 1;
@@ -602,7 +761,7 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
             __syncwarp();
           }
         }
-        double cum = wb;
+        double cum = wbl;
         int hit = -1;
         for (int e0 = 0; e0 < base && hit < 0; e0 += 32) {
           const int e = e0 + lane;
@@ -619,26 +778,27 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
           const SEnt h = ent[warp][hit];
           v = h.k == kZeroKey ? __ddiv_rn(P.Xc[j * n + h.row], P.pb[p * P.np + h.row]) : key64_inv(h.k);
           ok = true;
+        } else {  // the crossing lies above the interval
+          if (hi == ~0ULL) break;  // cannot happen: weights above sum to Tq
+          lo = hi + 1;
+          hi = ~0ULL;
         }
         __syncwarp();
-        if (!ok) break;  // cannot happen: the interval holds the crossing
       } else {
+        // narrow: exact weight per key bucket (integer-valued weights, so
+        // 64-bit integer shared atomics are exact and order-independent)
         int sh = (hi - lo == ~0ULL) ? 56 : ceil_log2_u64(hi - lo + 1) - 8;
         sh = sh > 0 ? sh : 0;
-        for (int b = lane; b < kSBins; b += 32) bins[warp][b] = 0.0;
+        for (int b = lane; b < kSBins; b += 32) bins[warp][b] = 0ULL;
         __syncwarp();
-        for (int64_t i = lane; i < n; i += 32) {
-          const double w = pwp[i];
-          if (w == 0.0) continue;
-          const unsigned long long k = key64(sratio<SAFE>(P, p, i, j));
-          // integer-valued doubles: exact, order-independent atomic sums
-          if (k >= lo && k <= hi) atomicAdd(&bins[warp][(k - lo) >> sh], w);
-        }
+        for_rows<SAFE>(P, p, j, lane, [&](bool okr, int, unsigned long long k, double w) {
+          if (okr && k >= lo && k <= hi) atomicAdd(&bins[warp][(k - lo) >> sh], (unsigned long long)w);
+        });
         __syncwarp();
-        double cum = wb;
+        double cum = wbl;
         int bsel = kSBins - 1;
         for (int b = 0; b < kSBins; ++b) {
-          const double hb = bins[warp][b];
+          const double hb = (double)bins[warp][b];
           if (cum + hb > G) { bsel = b; break; }
           cum += hb;
         }
@@ -647,7 +807,6 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
         if (nhi > hi || nhi < nlo) nhi = hi;
         lo = nlo;
         hi = nhi;
-        wb = cum;
         __syncwarp();
       }
     }
@@ -657,8 +816,10 @@ __global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
     }
     double e = 0.0;
     const double* pbp = P.pb + p * P.np;
-    for (int64_t i = lane; i < n; i += 32) e += fabs(__dsub_rn(P.Xc[j * n + i], __dmul_rn(pbp[i], v)));
-    for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+    const double* xc = P.Xc + j * n;
+#pragma unroll 4
+    for (int64_t i = lane; i < n; i += 32) e += fabs(__dsub_rn(xc[i], __dmul_rn(pbp[i], v)));
+    e = warp_sum(e);
     if (lane == 0) {
       P.V[kk * m + j] = v;
       P.E[kk * m + j] = e;

@@ -29,6 +29,10 @@ import torch
 from . import _lib
 
 RESCORE_RTOL = 1e-8
+# absolute part of the re-score window, times n*m*max|x|: device and NumPy
+# residual terms differ by a few ulps of |x_ij| + |v_j x_ip|, so a near-zero
+# objective (an exact fit) needs an absolute floor, not only a relative one
+RESCORE_ATOL = 1e-13
 
 
 def _stream_handle(stream: torch.cuda.Stream | None) -> int:
@@ -93,6 +97,7 @@ class DeviceFit:
 
     def prepare(self) -> None:
         """K0 (l1b_prepare); rerun whenever X changes."""
+        self._scale = None
         with torch.cuda.device(self.device):
             _lib.check(self.lib.l1b_prepare(self.X.data_ptr(), self.n, self.m, self.ws.data_ptr(),
                                             self.ws.numel(), self._s), "l1b_prepare")
@@ -117,6 +122,14 @@ class DeviceFit:
                 pen.data_ptr(), obj.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
         _lib.check(rc, "l1b_fit_pivots")
         return V, err, pen, obj
+
+    def straggler_counts(self, npiv: int | None = None) -> tuple[int, int]:
+        """Problems the last fit_pivots sent to the exact straggler solver."""
+        out = (ctypes.c_uint64 * 2)()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_fit_stats(self.n, self.m, npiv or self.max_pivots, self.ws.data_ptr(),
+                                              self.ws.numel(), ctypes.addressof(out), self._s), "l1b_fit_stats")
+        return int(out[0]), int(out[1])
 
     def residual_exact(self, v_dev: torch.Tensor, pivot: int) -> float:
         """residual_error (core.py:79-93) with NumPy's exact summation order."""
@@ -158,7 +171,9 @@ class DeviceFit:
             if math.isinf(best):
                 cand = np.nonzero(o == best)[0][:1]
             else:
-                cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + 1e-300)[0]
+                if self._scale is None:
+                    self._scale = self.absmax() * self.n * self.m
+                cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + RESCORE_ATOL * self._scale + 1e-300)[0]
             win = None
             for k in cand:  # ascending pivot order
                 p = p_begin + int(k) * p_stride

@@ -24,6 +24,15 @@ from paper_2402_16712_b200.engine import DeviceFit
 pytestmark = pytest.mark.gpu
 
 OBJ_RTOL = 1e-12
+# Per-pivot objectives are reduced in a fixed device order, not NumPy's, so
+# they match to rounding: relative 1e-12, plus an absolute floor of 1e-13 of
+# sum|X| for objectives that are (near) zero.  The winner's objective is
+# re-scored in NumPy's order and compared bit for bit.
+OBJ_ATOL = 1e-13
+
+
+def assert_obj_close(O, Oref, X, rtol=OBJ_RTOL):
+    np.testing.assert_allclose(O, Oref, rtol=rtol, atol=OBJ_ATOL * float(np.abs(X).sum()) + 1e-300)
 
 
 def _col_obj(X, p, j, t, lam):
@@ -112,7 +121,7 @@ def test_random_small_golden():
         _, V, E, P, O = _pivots(X, lams)
         V = V.transpose(1, 0, 2)  # [m][L][m] like the golden
         assert V.tobytes() == pV.tobytes(), t
-        np.testing.assert_allclose(O.T, pO, rtol=OBJ_RTOL, atol=1e-12)
+        assert_obj_close(O.T, pO, X)
         lines = l1b.fit_lines(X, lams)
         for k, line in enumerate(lines):
             assert line.preserved == lpiv[k], (t, k)
@@ -127,7 +136,7 @@ def test_c1_golden(tag):
     lams = g["lams"]
     _, V, E, P, O = _pivots(X, lams)
     assert V.transpose(1, 0, 2).tobytes() == g[f"{tag}_pV"].tobytes()
-    np.testing.assert_allclose(O.T, g[f"{tag}_pO"], rtol=OBJ_RTOL)
+    assert_obj_close(O.T, g[f"{tag}_pO"], X)
     for k, line in enumerate(l1b.fit_lines(X, lams)):
         assert line.preserved == g[f"{tag}_piv"][k]
         assert line.v.tobytes() == g[f"{tag}_v"][k].tobytes()
@@ -138,7 +147,7 @@ def test_grid_medium_golden():
     g = load_golden("grid_medium.npz")
     _, V, E, P, O = _pivots(g["X"], g["lams"])
     assert V.transpose(1, 0, 2).tobytes() == g["pV"].tobytes()
-    np.testing.assert_allclose(O.T, g["pO"], rtol=OBJ_RTOL)
+    assert_obj_close(O.T, g["pO"], g["X"])
     for k, line in enumerate(l1b.fit_lines(g["X"], g["lams"])):
         assert line.preserved == g["l_piv"][k] and line.objective == g["l_obj"][k]
 
@@ -174,7 +183,7 @@ def test_grid_data_bit_exact_vs_oracle(n, m, seed):
     _, V, E, P, O = _pivots(X, lams)
     Vo, Eo, Po, Oo = oracle.fit_pivots(X, lams)
     assert V.transpose(1, 0, 2).tobytes() == Vo.tobytes()
-    np.testing.assert_allclose(O.T, Oo, rtol=1e-11)
+    assert_obj_close(O.T, Oo, X, rtol=1e-11)
     for k, line in enumerate(l1b.fit_lines(X, lams)):
         want = oracle.fit_line(X, lams[k])
         assert line.preserved == want.preserved and line.v.tobytes() == want.v.tobytes()
@@ -224,7 +233,7 @@ def test_extreme_exponents_take_exact_division_path():
     for p in range(X.shape[1]):
         for k, lam in enumerate(lams):
             _assert_v_tie_aware(X, p, lam, V[k, p], Vo[p, k], "extreme")
-    np.testing.assert_allclose(O.T, Oo, rtol=1e-10)
+    assert_obj_close(O.T, Oo, X, rtol=1e-10)
 
 
 def test_raw_c2_shape_sampled_pivots_vs_oracle():

@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--lam", type=float, default=1.0)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--time", action="store_true")
 a = ap.parse_args()
 shapes = {"c1": (50, 200), "c2": (2000, 2000), "c4": (500, 100000), "c5": (10000, 10000)}
 m, n = shapes[a.config]
@@ -31,4 +32,14 @@ for _ in range(a.reps):
     V, E, P, O = eng.fit_pivots([a.lam], want_v=False)
 torch.cuda.synchronize()
 o = O.cpu().numpy()[0]
-print("best pivot", int(np.argmin(o)), float(o.min()))
+print("best pivot", int(np.argmin(o)), float(o.min()), "stragglers", eng.straggler_counts())
+if a.time:
+    ts = []
+    for _ in range(5):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        eng.fit_pivots([a.lam], want_v=False)
+        ev1.record()
+        ev1.synchronize()
+        ts.append(ev0.elapsed_time(ev1))
+    print("fit_pivots ms", sorted(ts))
