@@ -472,27 +472,38 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       const double* pyp = P.py + p * P.np;
       const double* pwp = P.pw + p * P.np;
       const unsigned long long KL = key64(Lw), KH = key64(Hw);
-      int nw = 0;
       double win = 0.0;
+      // phase 1: exact keys (independent L2 loads, unrolled for ILP);
+      // dropped rows and guard-band rows outside [Lw, Hw) get key ~0
+#pragma unroll 4
       for (int c = 0; c < cnt; ++c) {
         const int row = (int)cbuf[c * kBS + tid];
         const double a = xcol[row], b = pbp[row], y = pyp[row], w = pwp[row];
-        const double q = ratio_fast(a, b, y);
-        const unsigned long long k = key64(q);
-        if (w == 0.0 || k < KL || k >= KH) {  // dropped row, or a guard-band row outside the window
-          if (w != 0.0 && k < KL) wb += w;
-        } else {
+        unsigned long long k = key64(ratio_fast(a, b, y));
+        const bool inwin = w != 0.0 && k >= KL && k < KH;
+        if (w != 0.0 && k < KL) wb += w;
+        if (inwin) {
           es -= fabs(__fma_rn(-b, c0, a));  // pass B added every row
           win += w;
-          int d = nw++;
-          while (d > 0 && key[(d - 1) * kBS + tid] > k) {
-            key[d * kBS + tid] = key[(d - 1) * kBS + tid];
-            cbuf[d * kBS + tid] = cbuf[(d - 1) * kBS + tid];
-            --d;
-          }
-          key[d * kBS + tid] = k;
-          cbuf[d * kBS + tid] = (RowT)row;
+        } else {
+          k = ~0ULL;
         }
+        key[c * kBS + tid] = k;
+      }
+      // phase 2: stable insertion of the window rows by key, in place
+      int nw = 0;
+      for (int c = 0; c < cnt; ++c) {
+        const unsigned long long k = key[c * kBS + tid];
+        if (k == ~0ULL) continue;
+        const RowT row = cbuf[c * kBS + tid];
+        int d = nw++;
+        while (d > 0 && key[(d - 1) * kBS + tid] > k) {
+          key[d * kBS + tid] = key[(d - 1) * kBS + tid];
+          cbuf[d * kBS + tid] = cbuf[(d - 1) * kBS + tid];
+          --d;
+        }
+        key[d * kBS + tid] = k;
+        cbuf[d * kBS + tid] = row;
       }
       if (wb <= G && G < wb + win) {
         double cum = wb;
@@ -593,7 +604,7 @@ __global__ void k_queue_all(SelParams P) {
 // SAFE, IEEE __ddiv_rn otherwise.
 
 constexpr int kSWarps = 8;
-constexpr int kSCap = 256;   // interval elements collected and sorted per round
+constexpr int kSCap = 128;   // interval elements collected and sorted per round
 constexpr int kSBins = 256;  // radix bins when the interval holds more
 constexpr int kSUnroll = 4;  // rows per lane in flight (loads hoisted for ILP)
 
@@ -650,7 +661,7 @@ __device__ __forceinline__ void for_rows(const SelParams& P, int64_t p, int64_t 
 }
 
 template <bool SAFE>
-__global__ void __launch_bounds__(kSWarps * 32) k_straggle(SelParams P) {
+__global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
   extern __shared__ __align__(16) unsigned char ssm[];
   SEnt(*ent)[kSCap] = reinterpret_cast<SEnt(*)[kSCap]>(ssm);
   unsigned long long(*bins)[kSBins] =
