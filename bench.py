@@ -49,8 +49,10 @@ CONFIGS = {
     "c1": ("outlier", 50, 200, [0.1], "synthetic 200x50 + 10% outliers, lambda=0.1"),
     "c2": ("line", 2000, 2000, [1.0], "paper benchmark 2000x2000 synthetic, lambda=1"),
     "c3": ("line", 2000, 2000, None, "lambda sweep of 32 penalties on 2000x2000"),
+    "c4": ("line", 500, 100000, [1.0], "tall 100000x500, 3 components via deflation"),
     "c5": ("line", 10000, 10000, [1.0], "10000x10000, pivots sharded across GPUs"),
 }
+COMPONENTS = {"c4": 3}
 METRIC = "ms per sparse L1 line fit at 2000×2000 and weighted-median solves/sec vs CPU"
 
 
@@ -190,9 +192,22 @@ def _config_dict(args, X, lams, world):
     n, m = X.shape
     return {"workload": args.config, "description": CONFIGS[args.config][4], "n": n, "m": m,
             "n_lambdas": len(lams), "lambda": lams[0] if len(lams) == 1 else [lams[0], lams[-1]],
-            "solves_per_fit": m * (m - 1) * len(lams), "ratio_elements_per_fit": m * (m - 1) * n,
+            "components": COMPONENTS.get(args.config, 1),
+            "solves_per_step": m * (m - 1) * len(lams) * COMPONENTS.get(args.config, 1),
+            "ratio_elements_per_fit": m * (m - 1) * n,
             "parallelism": f"pivot-shard x{world}" if world > 1 else "1 gpu",
             "l2": "flushed (256 MB write) before every timed step"}
+
+
+def _sync_time(stream, fn):
+    """Device time of fn() on `stream` with CUDA events (ms) and its result."""
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    out = fn()
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b), out
 
 
 def run_ours(args):
@@ -212,18 +227,32 @@ def run_ours(args):
     lib = _lib.load()
     X, lams = _make_data(args.config)
     n, m = X.shape
+    ncomp = COMPONENTS.get(args.config, 1)
     p_begin, p_stride, npiv = shard(m, rank, world)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     eng = DeviceFit(X, device=dev, max_pivots=max(1, npiv))
+    X0 = eng.X.clone() if ncomp > 1 else None
 
     def step():
+        """One workload pass with X resident: fit_line (every lambda), or
+        fit_subspace's fit -> deflate loop (subspace.py:54-76) for C4."""
+        if X0 is not None:
+            eng.X.copy_(X0)
         eng.prepare()
-        wins = eng.shard_winners(lams, p_begin, p_stride, npiv)
-        if world > 1:
-            wins = combine_winners(wins, m)
-        return wins
+        out = []
+        scale = max(1.0, eng.absmax()) if ncomp > 1 else 1.0
+        for t in range(ncomp):
+            if ncomp > 1 and eng.absmax() <= 1e-10 * scale:
+                break
+            wins = eng.shard_winners(lams, p_begin, p_stride, npiv)
+            if world > 1:
+                wins = combine_winners(wins, m)
+            out.append(wins)
+            if t + 1 < ncomp:
+                eng.deflate(wins[0].v)
+        return out
 
     def barrier():
         if world > 1:
@@ -239,12 +268,8 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            wins = step()
-            b.record(stream)
-            b.synchronize()
-            times.append(a.elapsed_time(b))
+            ms, res = _sync_time(stream, step)
+            times.append(ms)
     barrier()
     launches = (lib.l1b_kernel_launches() - launches0) / args.steps
     ms_local = float(np.sum(times))
@@ -252,63 +277,58 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms_total = float(tot.item())
-    solves = m * (m - 1) * len(lams) * args.steps
-    value = solves / (ms_total / 1e3)
+    solves_step = m * (m - 1) * len(lams) * ncomp
+    value = solves_step * args.steps / (ms_total / 1e3)
 
-    # ---- dominant kernel: k_select alone, event-timed on the same stream ---
+    # ---- dominant kernel: K1 (k_select + stragglers) alone, same stream ----
+    if X0 is not None:
+        eng.X.copy_(X0)
+    eng.prepare()
     sel_ms = []
     for _ in range(max(3, min(args.steps, 5))):
         flush.fill_(1)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        eng.fit_pivots(lams, p_begin, p_stride, npiv, want_v=False)
-        b.record(stream)
-        b.synchronize()
-        sel_ms.append(a.elapsed_time(b))
+        ms, _ = _sync_time(stream, lambda: eng.fit_pivots(lams, p_begin, p_stride, npiv, want_v=False))
+        sel_ms.append(ms)
     sel_ms = float(np.median(sel_ms))
+    strag = eng.straggler_counts(npiv)[0]
 
     # ---- FP64 peak probe ---------------------------------------------------
     probe = torch.zeros(1, dtype=torch.float64, device=dev)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     iters, blocks, thr = 1 << 14, nsm * 8, 256
     _lib.check(lib.l1b_dfma_probe(iters, blocks, thr, probe.data_ptr(), stream.cuda_stream), "probe")
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    _lib.check(lib.l1b_dfma_probe(iters, blocks, thr, probe.data_ptr(), stream.cuda_stream), "probe")
-    b.record(stream)
-    b.synchronize()
-    fp64_ops = 8.0 * iters * blocks * thr / (a.elapsed_time(b) / 1e3)  # DFMA per second
+    pms, _ = _sync_time(stream, lambda: _lib.check(
+        lib.l1b_dfma_probe(iters, blocks, thr, probe.data_ptr(), stream.cuda_stream), "probe"))
+    fp64_ops = 8.0 * iters * blocks * thr / (pms / 1e3)  # DFMA per second
 
-    elems = npiv * (m - 1) * n * len(lams)  # ratio elements this rank's select launches touch
+    elems = npiv * (m - 1) * n * len(lams)  # ratio elements one fit_pivots call covers on this rank
     achieved = 11.0 * elems / (sel_ms / 1e3)
 
-    # ---- end to end through the public API --------------------------------
-    e2e_ms = []
-    Xh = np.ascontiguousarray(X)
+    # ---- end to end through the public API (host numpy in, FittedLine out) --
+    data = l1b.DataMatrix(X)  # built once, as the reference CLI does before timing fit_line
     if world == 1:
-        for k in range(args.warmup + args.steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            lines = l1b.fit_lines(Xh, lams)
-            b.record(stream)
-            b.synchronize()
-            if k >= args.warmup:
-                e2e_ms.append(a.elapsed_time(b))
-        e2e_val = solves / (float(np.sum(e2e_ms)) / 1e3)
+        def e2e_step():
+            if ncomp > 1:
+                return l1b.fit_subspace(data, lams[0], ncomp)
+            return l1b.fit_lines(data, lams)
     else:
-        from paper_2402_16712_b200.distributed import fit_lines_distributed
-        for k in range(args.warmup + args.steps):
-            dist.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            lines = fit_lines_distributed(Xh, lams)
-            b.record(stream)
-            b.synchronize()
-            if k >= args.warmup:
-                e2e_ms.append(a.elapsed_time(b))
-        t = torch.tensor([float(np.sum(e2e_ms))], dtype=torch.float64, device=dev)
+        from paper_2402_16712_b200.distributed import fit_lines_distributed, fit_subspace_distributed
+
+        def e2e_step():
+            if ncomp > 1:
+                return fit_subspace_distributed(data, lams[0], ncomp)
+            return fit_lines_distributed(data, lams)
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        barrier()
+        ms, res = _sync_time(stream, e2e_step)
+        if k >= args.warmup:
+            e2e_ms.append(ms)
+    lines = list(res.components) if ncomp > 1 else res
+    t = torch.tensor([float(np.sum(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_val = solves / (float(t.item()) / 1e3)
+    e2e_val = solves_step * args.steps / (float(t.item()) / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -326,12 +346,14 @@ def run_ours(args):
             "result": {"pivot": [l.preserved for l in lines][:4], "objective": [l.objective for l in lines][:4],
                        "nonzeros": [int(np.count_nonzero(l.v)) for l in lines][:4]},
             "e2e": {"value": e2e_val, "unit": "solves/s", "ms_per_step": float(np.mean(e2e_ms)),
-                    "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(8 * m * len(lams) + 8 * npiv * len(lams))},
+                    "h2d_bytes_per_step": int(X.nbytes),
+                    "d2h_bytes_per_step": int(8 * m * len(lams) * ncomp + 8 * npiv * len(lams) * ncomp)},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": "k_select", "achieved": achieved / 1e12,
+            "roofline": {"bound": "fp64", "kernel": "k_select+k_straggle (K1)", "achieved": achieved / 1e12,
                          "peak": fp64_ops / 1e12, "unit": "TOP/s (FP64 pipe ops)",
                          "frac": achieved / fp64_ops, "traffic": None,
                          "kernel_ms": sel_ms, "ops_per_element": 11, "elements_per_launch": elems,
+                         "stragglers_per_launch": strag,
                          "peak_source": "measured: l1b_dfma_probe (DFMA/s, 1 op per DFMA)",
                          "hbm_view": {"algorithmic_bytes": int(8 * n * m), "achieved_GBs": 8 * n * m / (sel_ms / 1e3) / 1e9,
                                       "peak_GBs": _peak_hbm()}},

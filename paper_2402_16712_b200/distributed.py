@@ -28,7 +28,8 @@ import torch.distributed as dist
 from .core import FittedLine
 from .engine import DeviceFit, PivotWinner, shard
 
-__all__ = ["shard", "combine_winners", "fit_lines_distributed", "fit_line_distributed"]
+__all__ = ["shard", "combine_winners", "fit_lines_distributed", "fit_line_distributed",
+           "fit_subspace_distributed"]
 
 
 def _comm_device(group=None) -> torch.device:
@@ -109,3 +110,38 @@ def fit_lines_distributed(X, lams, group=None,
 
 def fit_line_distributed(X, lam: float, group=None, solver: Callable | None = None) -> FittedLine:
     return fit_lines_distributed(X, [lam], group, solver)[0]
+
+
+def fit_subspace_distributed(data, lam: float, k: int, group=None):
+    """fit_subspace (subspace.py:54-76) with every component's pivots sharded.
+
+    Each rank keeps its own device replica of X; after the winner of a
+    component is combined, every rank deflates its replica with the same v
+    (subspace.py:22-36), so the replicas stay bit-identical with no traffic
+    beyond the winner exchange.
+    """
+    import math
+
+    from .core import SubspaceFit
+
+    X = np.ascontiguousarray(getattr(data, "values", data), dtype=np.float64)
+    n, m = X.shape
+    if not 1 <= k < m:
+        raise ValueError(f"component count {k} must be in [1, {m - 1}]")
+    if lam < 0.0 or not math.isfinite(lam):
+        raise ValueError("penalty weight must be finite and nonnegative")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    p_begin, p_stride, npiv = shard(m, rank, world)
+    eng = DeviceFit(X, max_pivots=max(1, npiv))
+    scale = max(1.0, eng.absmax())
+    comps = []
+    for t in range(k):
+        if eng.absmax() <= 1e-10 * scale:
+            return SubspaceFit(tuple(comps), degenerate=True)
+        local = eng.shard_winners([float(lam)], p_begin, p_stride, npiv) if npiv > 0 else [None]
+        w = combine_winners(local, m, group)[0]
+        comps.append(FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,
+                                penalty_norm=w.penalty_norm, objective=w.objective))
+        if t + 1 < k:
+            eng.deflate(w.v)
+    return SubspaceFit(tuple(comps), degenerate=False)

@@ -56,6 +56,20 @@ def _pivots(X, lams, **kw):
     return eng, V.cpu().numpy(), E.cpu().numpy(), P.cpu().numpy(), O.cpu().numpy()
 
 
+@pytest.mark.parametrize("n,m", [(1, 3), (37, 11), (3000, 7001), (100000, 500)])
+def test_residual_exact_matches_numpy_bits(n, m):
+    """l1b_residual_exact == residual_error (core.py:93) bit for bit, up to C4's n*m."""
+    rng = np.random.default_rng(n + m)
+    X = rng.standard_normal((n, m))
+    v = rng.standard_normal(m)
+    p = m // 2
+    v[p] = 1.0
+    want = float(np.abs(X - np.outer(X[:, p], v)).sum())
+    eng = DeviceFit(X, max_pivots=1)
+    got = eng.residual_exact(torch.from_numpy(v).to(eng.device), p)
+    assert got == want, (got, want)
+
+
 def test_division_selftest_bit_exact():
     eng = DeviceFit(TOY)
     assert eng.selftest_divide(n_pairs=1 << 28, seed=7) == 0
