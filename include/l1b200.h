@@ -101,6 +101,12 @@ int l1b_selftest_divide(uint64_t seed, int64_t n_pairs, uint64_t* d_mismatches, 
 int l1b_fit_stats(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes,
                   uint64_t* h_out, void* stream);
 
+/* Profiling aid (no reference counterpart): when d_buf is non-NULL, every
+ * later k_select launch writes per-CTA %globaltimer stamps at its phase
+ * boundaries (sample, F passes, pass B, resolve) into d_buf[cta * 8 + k];
+ * d_buf must hold 8 * (number of CTAs) uint64.  NULL switches it off. */
+int l1b_set_probe(uint64_t* d_buf);
+
 /* Cumulative count of kernels this library has enqueued in the process
  * (benchmark evidence for "gpu_launches"; no reference counterpart). */
 uint64_t l1b_kernel_launches(void);

@@ -29,6 +29,7 @@ ABI_SYMBOLS = (
     "l1b_kernel_launches",
     "l1b_dfma_probe",
     "l1b_fit_stats",
+    "l1b_set_probe",
 )
 
 L1B_OK = 0
@@ -88,6 +89,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_dfma_probe.argtypes = [_i64, _i32, _i32, _vp, _vp]
     lib.l1b_fit_stats.restype = ctypes.c_int
     lib.l1b_fit_stats.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _vp]
+    lib.l1b_set_probe.restype = ctypes.c_int
+    lib.l1b_set_probe.argtypes = [_vp]
     _lib = lib
     return lib
 

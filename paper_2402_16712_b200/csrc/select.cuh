@@ -46,6 +46,7 @@ struct SelParams {
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float |x_ip|) in 8-pivot groups
   const double* Xc;      // column-major m x n
+  const PRec* prec;      // [m][np] (x_ip, y_ip, wq_ip) records
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
   const double* pw;      // [m][n] fixed-point weight (exact integer)
@@ -63,6 +64,15 @@ struct SelParams {
   Straggler* strag;
   unsigned long long* nstrag;
   int* status;
+  unsigned long long* tprobe;  // optional [grid][8] phase timestamps (profiling builds; null = off)
+  // window records, k_select -> k_resolve (problem index kk * m + j)
+  double* rG;
+  double* rwb;
+  double* res;
+  double* rLw;
+  double* rHw;
+  int* rcnt;
+  unsigned char* rrows;  // RowT [CAP][npiv*m]
 };
 
 // acc += x if p, exactly (x, acc integer-valued): one select of the high
@@ -70,6 +80,11 @@ struct SelParams {
 // compiler's if-conversion emits.
 __device__ __forceinline__ void padd(double& acc, double x, bool p) {
   acc = __fma_rn(x, __hiloint2double(p ? 0x3ff00000 : 0, 0), acc);
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
 }
 
 // Exact region test: returns false for a dead column, else sets G.  All
@@ -211,6 +226,11 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   auto pF = [&](const unsigned char* b, const StageLayout& L) { return (const float2*)(b + L.pf) + warp; };
   auto pBW = [&](const unsigned char* b, const StageLayout& L) { return (const double2*)(b + L.bw) + warp; };
 
+  unsigned long long* tp = P.tprobe ? P.tprobe + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 : nullptr;
+  auto stamp = [&](int k) {
+    if (tp && tid == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); tp[k] = t; }
+  };
+  stamp(0);
   // ---- sample: float ratios of 32 strided rows, sorted -> value bracket ----
   float lo = 0.f, hi = 0.f;
   if (active) {
@@ -271,6 +291,8 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     hi += e;
   }
 
+  __syncthreads();
+  stamp(1);
   // ---- F passes: 64-slot FP32 histograms, each narrowing the range ---------
   // slot(r) = RN(63 * sat(r * A + B)): slot 0 <-> r < lo, slot b in 1..62 <->
   // r in [lo + (b-1) w, lo + b w) with w = (hi - lo) / 62, slot 63 <-> r >= hi
@@ -292,29 +314,68 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     for (int b = 0; b < kNB; ++b) hist[b * kBS + tid] = 0.f;
     const unsigned hbase = smem_u32(hist + tid) - 0x4B000000u * (unsigned)(kBS * 4);
     const bool busy = __any_sync(0xffffffffu, live);
-    // the histogram update shared by every variant; returns the slot bits
-    auto bin = [&](float q, float wgt) {
-      const float u = __saturatef(fmaf(q, A, B));
-      const unsigned bits = __float_as_uint(fmaf(u, 63.f, 8388608.f));
-      const unsigned addr = hbase + bits * (unsigned)(kBS * 4);
-      float h;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h) : "r"(addr));
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(h + wgt));
-      return bits;
+    // One F pass over a staged chunk, all kRows rows (pad rows past n have
+    // y = w = wq = 0 and add nothing).  Rows go in batches of 4: the tile and
+    // plane loads and slot arithmetic of a batch are issued first, then the
+    // four histogram read-modify-writes, whose program order (volatile asm)
+    // keeps same-slot updates correct -- so only the RMWs, not the loads,
+    // form the serial chain.  KIND 0: float single pass (+ float Wneg);
+    // 1: exact first pass (+ exact Wneg and slot-0 weight); 2: exact later
+    // pass (+ slot-0 weight).
+    float wn32 = 0.f;
+    double wlow = 0.0;
+    auto fbody = [&](const unsigned char* sb, const StageLayout& L, auto kind) {
+      constexpr int K = decltype(kind)::value;
+      const float* ta = tF(sb, L);
+      const float2* pf = pF(sb, L);
+      const double2* bw = pBW(sb, L);
+#pragma unroll 2
+      for (int r0 = 0; r0 < kRows; r0 += 4) {
+        float2 yw[4];
+        float av[4];
+        double wq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          yw[u] = pf[(r0 + u) * 8];
+          av[u] = ta[(r0 + u) * 32 + lane];
+          if (K != 0) wq[u] = bw[(r0 + u) * 8].y;
+        }
+        unsigned addr[4];
+        float q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          q[u] = av[u] * yw[u].x;
+          const float uu = __saturatef(fmaf(q[u], A, B));
+          addr[u] = hbase + __float_as_uint(fmaf(uu, 63.f, 8388608.f)) * (unsigned)(kBS * 4);
+        }
+        // the four slot reads go out together; a row whose slot an earlier
+        // row of the batch also hit adds that row's weight too, and the
+        // stores go in row order, so the last store to a slot carries every
+        // update -- no read waits for a store
+        float h[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h[u]) : "r"(addr[u]));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float t = h[u] + yw[u].y;
+#pragma unroll
+          for (int v = 0; v < u; ++v)
+            asm("{\n .reg .pred e;\n setp.eq.u32 e, %1, %2;\n @e add.f32 %0, %0, %3;\n}"
+                : "+f"(t) : "r"(addr[u]), "r"(addr[v]), "f"(yw[v].y));
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(t));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (K == 0 && q[u] < 0.f) wn32 += yw[u].y;
+          if (K == 1) padd(wneg, wq[u], q[u] < 0.f);                     // exact: signs of q32 are exact
+          if (K != 0) padd(wlow, wq[u], addr[u] == hbase + 0x4B000000u * (unsigned)(kBS * 4));  // slot 0
+        }
+      }
     };
     double base;
     if (!exact_f) {  // single float pass (pass == 0)
-      float wn32 = 0.f;
-      sweep(W_F | W_PF, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-        const float* ta = tF(sb, L);
-        const float2* pf = pF(sb, L);
-#pragma unroll 4
-        for (int r = 0; r < rmax; ++r) {
-          const float2 yw = pf[r * 8];
-          const float q = ta[r * 32 + lane] * yw.x;
-          bin(q, yw.y);
-          if (q < 0.f) wn32 += yw.y;
-        }
+      sweep(W_F | W_PF, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+        fbody(sb, L, std::integral_constant<int, 0>{});
       });
       float T32 = 0.f;
 #pragma unroll
@@ -326,35 +387,14 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       if (fabsf(D32) + 1e-7f * (float)n * T32 < lam32 * (1.f - 1e-6f)) live = false;
       base = (double)hist[tid];
     } else if (pass == 0) {
-      double wlow = 0.0;
-      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-        const float* ta = tF(sb, L);
-        const float2* pf = pF(sb, L);
-        const double2* bw = pBW(sb, L);
-#pragma unroll 4
-        for (int r = 0; r < rmax; ++r) {
-          const float2 yw = pf[r * 8];
-          const float q = ta[r * 32 + lane] * yw.x;
-          const unsigned bits = bin(q, yw.y);
-          const double wq = bw[r * 8].y;
-          padd(wneg, wq, q < 0.f);                 // exact: signs of q32 are exact
-          padd(wlow, wq, bits == 0x4B000000u);     // exact weight of slot 0
-        }
+      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+        fbody(sb, L, std::integral_constant<int, 1>{});
       });
       if (live && !region_G(Tq, wneg, Lsc, &G)) live = false;  // dead column
       base = wlow * unit;
     } else {
-      double wlow = 0.0;
-      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t) {
-        const float* ta = tF(sb, L);
-        const float2* pf = pF(sb, L);
-        const double2* bw = pBW(sb, L);
-#pragma unroll 4
-        for (int r = 0; r < rmax; ++r) {
-          const float2 yw = pf[r * 8];
-          const float q = ta[r * 32 + lane] * yw.x;
-          padd(wlow, bw[r * 8].y, bin(q, yw.y) == 0x4B000000u);  // exact weight below the range
-        }
+      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+        fbody(sb, L, std::integral_constant<int, 2>{});
       });
       base = wlow * unit;
     }
@@ -398,6 +438,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     }
   }
 
+  stamp(2);
   // ---- pass B: exact weights + fused residual; the window is collected -----
   // Float ratios carry < 2^-21 relative error, so an element whose float
   // ratio is below Lg (Lw less a guard band) is certainly below the window
@@ -423,23 +464,34 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     const float2* pf = pF(sb, L);
     const double2* bwp = pBW(sb, L);
     const double* xa = tA(sb, L);
-#pragma unroll 4
-    for (int r = 0; r < rmax; ++r) {
-      const float q32 = ta[r * 32 + lane] * pf[r * 8].x;
-      const double2 bw = bwp[r * 8];  // (x_ip, wq)
-      const double a = xa[r * 32 + lane];
-      if (decltype(want_wneg)::value) padd(wneg, bw.y, q32 < 0.f);
-      const bool below = q32 < Lg;
-      const bool inw = !below && q32 < Hg;
-      padd(wb, bw.y, below);
-      if (inw && cnt < CAP) {
-        const unsigned addr = cb0 + (unsigned)(cnt * kBS * sizeof(RowT));
-        const RowT row = (RowT)(i0 + r);
-        if (sizeof(RowT) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)row));
-        else asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"((unsigned)row));
+    // batches of 4 rows: loads first, then the (branch-free) bookkeeping;
+    // pad rows past n (all zeros) add nothing and are never collected
+#pragma unroll 2
+    for (int r0 = 0; r0 < kRows; r0 += 4) {
+      float q32[4];
+      double2 bw[4];
+      double a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        q32[u] = ta[(r0 + u) * 32 + lane] * pf[(r0 + u) * 8].x;
+        bw[u] = bwp[(r0 + u) * 8];  // (x_ip, wq)
+        a[u] = xa[(r0 + u) * 32 + lane];
       }
-      cnt += inw;
-      es += fabs(__fma_rn(-bw.x, c0, a));  // the resolve takes the window rows back out
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (decltype(want_wneg)::value) padd(wneg, bw[u].y, q32[u] < 0.f);
+        const bool below = q32[u] < Lg;
+        const bool inw = (!below) & (q32[u] < Hg) & (r0 + u < rmax);  // bitwise: no branches
+        padd(wb, bw[u].y, below);
+        if (inw & (cnt < CAP)) {
+          const unsigned addr = cb0 + (unsigned)(cnt * kBS * sizeof(RowT));
+          const RowT row = (RowT)(i0 + r0 + u);
+          if (sizeof(RowT) == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)row));
+          else asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"((unsigned)row));
+        }
+        cnt += inw;
+        es += fabs(__fma_rn(-bw[u].x, c0, a[u]));  // the resolve takes the window rows back out
+      }
     }
   };
   const bool busyB = __any_sync(0xffffffffu, live);
@@ -452,104 +504,50 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       bbody(sb, L, rmax, i0, std::true_type{});
     });
   __syncthreads();  // the ring (incl. the histogram space) is free for the resolve keys
+  stamp(3);
 
   if (live && !exact_f && !region_G(Tq, wneg, Lsc, &G)) live = false;  // exact dead test
   double v = 0.0, e = 0.0;
   bool done = !active;
-  unsigned long long slo = 0, shi = ~0ULL;  // straggler interval
-  if (active) {
-    if (!live) {
-      done = true;  // dead column (fit.py:60-63 returns +0.0): residual = sum_i |x_ij|
-      e = P.colsum[j];
-    } else if (cnt <= CAP) {
-      // resolve: exact keys of the collected rows; guard-band rows below Lw /
-      // at or above Hw join the sides, the rest (the window) is sorted by
-      // (key, row) -- stable insertion, rows were collected in ascending
-      // order -- and walked to the crossing
-      unsigned long long* key = (unsigned long long*)hist;  // [CAP][kBS]
-      const double* xcol = P.Xc + jc * n;
-      const double* pbp = P.pb + p * P.np;
-      const double* pyp = P.py + p * P.np;
-      const double* pwp = P.pw + p * P.np;
-      const unsigned long long KL = key64(Lw), KH = key64(Hw);
-      double win = 0.0;
-      // phase 1: exact keys (independent L2 loads, unrolled for ILP);
-      // dropped rows and guard-band rows outside [Lw, Hw) get key ~0
-#pragma unroll 4
-      for (int c = 0; c < cnt; ++c) {
-        const int row = (int)cbuf[c * kBS + tid];
-        const double a = xcol[row], b = pbp[row], y = pyp[row], w = pwp[row];
-        unsigned long long k = key64(ratio_fast(a, b, y));
-        const bool inwin = w != 0.0 && k >= KL && k < KH;
-        if (w != 0.0 && k < KL) wb += w;
-        if (inwin) {
-          es -= fabs(__fma_rn(-b, c0, a));  // pass B added every row
-          win += w;
-        } else {
-          k = ~0ULL;
-        }
-        key[c * kBS + tid] = k;
-      }
-      // phase 2: stable insertion of the window rows by key, in place
-      int nw = 0;
-      for (int c = 0; c < cnt; ++c) {
-        const unsigned long long k = key[c * kBS + tid];
-        if (k == ~0ULL) continue;
-        const RowT row = cbuf[c * kBS + tid];
-        int d = nw++;
-        while (d > 0 && key[(d - 1) * kBS + tid] > k) {
-          key[d * kBS + tid] = key[(d - 1) * kBS + tid];
-          cbuf[d * kBS + tid] = cbuf[(d - 1) * kBS + tid];
-          --d;
-        }
-        key[d * kBS + tid] = k;
-        cbuf[d * kBS + tid] = row;
-      }
-      if (wb <= G && G < wb + win) {
-        double cum = wb;
-        for (int c = 0; c < nw && !done; ++c) {
-          const int row = (int)cbuf[c * kBS + tid];
-          cum += pwp[row];
-          if (cum > G) {
-            const unsigned long long k = key[c * kBS + tid];
-            v = k == kZeroKey ? __ddiv_rn(xcol[row], pbp[row]) : key64_inv(k);
-            done = true;
-          }
-        }
-        double ew = 0.0;
-        for (int c = 0; c < nw; ++c) {
-          const int row = (int)cbuf[c * kBS + tid];
-          ew += fabs(__dsub_rn(xcol[row], __dmul_rn(pbp[row], v)));  // core.py:93 rounding
-        }
-        const double wa = Tq - wb - win;  // exact
-        e = es + ew + (v - c0) * ((wb - wa) * unit);
-      } else if (G < wb) {  // exact weights put the crossing below / above the window
-        slo = 0;
-        shi = KL - 1;
-      } else {
-        slo = KH;
-        shi = ~0ULL;
-      }
-    } else {
-      // window overflow (heavy ties / wide window): the crossing is most
-      // likely in [Lg, Hg); the straggler solver widens the interval itself
-      // if it is not
-      slo = key64((double)Lg - fabs((double)Lg) * 0x1p-20);
-      shi = key64((double)Hg + fabs((double)Hg) * 0x1p-20);
-    }
-    if (!done) {
-      Straggler s;
-      s.kk = (int)kk;
-      s.j = (int)j;
-      s.G = G;
-      s.lo = slo;
-      s.hi = shi;
-      s.wb = 0.0;
-      unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
-      P.strag[slot] = s;
+  if (active && !live) {
+    done = true;  // dead column (fit.py:60-63 returns +0.0): residual = sum_i |x_ij|
+    e = P.colsum[j];
+  }
+  // hand the window to k_resolve (its exact keys need scattered L2 loads, so
+  // it runs as its own high-occupancy kernel instead of holding this CTA's
+  // shared memory), or an overflowing window to the straggler solver
+  if (piv_ok && j < m) {
+    const int64_t prob = kk * m + j;
+    const int64_t NP = P.npiv * m;
+    const bool rec = active && live && cnt <= CAP;
+    P.rcnt[prob] = rec ? cnt : -1;
+    if (rec) {
+      P.rG[prob] = G;
+      P.rwb[prob] = wb;
+      P.res[prob] = es;
+      P.rLw[prob] = Lw;
+      P.rHw[prob] = Hw;
+      RowT* rows = (RowT*)P.rrows;
+      for (int c = 0; c < cnt; ++c) rows[c * NP + prob] = cbuf[c * kBS + tid];
+      done = true;  // k_resolve writes V / E (or queues a straggler)
     }
   }
+  if (active && live && cnt > CAP) {
+    // window overflow (heavy ties / wide window): the crossing is most likely
+    // in [Lg, Hg); the straggler solver widens the interval itself if not
+    Straggler s;
+    s.kk = (int)kk;
+    s.j = (int)j;
+    s.G = G;
+    s.lo = key64((double)Lg - fabs((double)Lg) * 0x1p-20);
+    s.hi = key64((double)Hg + fabs((double)Hg) * 0x1p-20);
+    s.wb = 0.0;
+    unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
+    P.strag[slot] = s;
+  }
 
+  __syncthreads();
+  stamp(4);
   if (piv_ok && j < m) {
     if (degenerate) {
       P.V[kk * m + j] = 0.0;
@@ -557,11 +555,128 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     } else if (j == p) {
       P.V[kk * m + j] = 1.0;
       P.E[kk * m + j] = 0.0;
-    } else if (done) {
+    } else if (active && !live) {
       P.V[kk * m + j] = v;
       P.E[kk * m + j] = e;
     }
   }
+}
+
+// ---------------------------------------------------------------- resolve --
+//
+// One thread per (pivot, target) problem with a window record from
+// k_select: exact keys of the collected rows (loads batched for ILP, the
+// kernel runs at high occupancy to hide the L2 latency), guard-band rows
+// below Lw / at or above Hw join the sides, the window rows are sorted by
+// (key, row) -- stable insertion; rows were collected in ascending order --
+// and walked to the crossing.  Residual: pass B summed |x_ij - c0 x_ip| over
+// every row; the window rows are taken back out and re-added as
+// |x_ij - fl(v x_ip)| (core.py:93 rounding), and the sides move from c0 to v
+// by (v - c0)(W_below - W_above) exactly as in the pass-B identity.
+
+constexpr int kRBS = 128;  // threads per k_resolve block
+
+template <typename RowT, int CAP>
+constexpr size_t resolve_smem() {
+  return (size_t)kRBS * CAP * (2 * sizeof(double) + 1);
+}
+
+template <typename RowT, int CAP>
+__global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  unsigned long long* key = (unsigned long long*)rsm;             // [CAP][kRBS]
+  double* kw = (double*)(rsm + (size_t)kRBS * CAP * 8);           // [CAP][kRBS] weight
+  unsigned char* kc = rsm + (size_t)kRBS * CAP * 16;              // [CAP][kRBS] collection index
+  const int tid = threadIdx.x;
+  const int64_t NP = P.npiv * P.m;
+  const int64_t prob = (int64_t)blockIdx.x * kRBS + tid;
+  if (prob >= NP) return;
+  const int cnt = P.rcnt[prob];
+  if (cnt < 0) return;
+  const int64_t m = P.m, n = P.n;
+  const int64_t kk = prob / m, j = prob - kk * m;
+  const int64_t p = P.p_begin + kk * P.p_stride;
+  const double G = P.rG[prob], Lw = P.rLw[prob], Hw = P.rHw[prob];
+  double wb = P.rwb[prob], es = P.res[prob];
+  const double c0 = Lw > -kBig ? Lw : Hw;
+  const double Tq = P.tq[p];
+  const double unit = ldexp(1.0, -P.spow[p]);
+  const double* xcol = P.Xc + j * n;
+  const PRec* pr = P.prec + p * P.np;
+  const RowT* rows = (const RowT*)P.rrows;
+  const unsigned long long KL = key64(Lw), KH = key64(Hw);
+  double win = 0.0;
+  // phase 1: exact keys (two L2 sectors per row: x_ij and the pivot record),
+  // four rows in flight; guard-band rows outside [Lw, Hw) and dropped rows
+  // are settled here, the window rows kept as (key, weight)
+  int nw = 0;
+  for (int c0i = 0; c0i < cnt; c0i += 4) {
+    double a[4];
+    double2 by[4], wz[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = c0i + u < cnt;
+      const int row = ok ? (int)rows[(c0i + u) * NP + prob] : 0;
+      a[u] = ok ? xcol[row] : 0.0;
+      by[u] = ok ? reinterpret_cast<const double2*>(pr + row)[0] : make_double2(0.0, 0.0);
+      wz[u] = ok ? reinterpret_cast<const double2*>(pr + row)[1] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0i + u >= cnt) break;
+      const double w = wz[u].x;
+      const unsigned long long k = key64(ratio_fast(a[u], by[u].x, by[u].y));
+      if (w == 0.0) continue;  // dropped row: |x_ij| already in es
+      if (k < KL) { wb += w; continue; }
+      if (k >= KH) continue;
+      es -= fabs(__fma_rn(-by[u].x, c0, a[u]));  // pass B added every row
+      win += w;
+      // stable insertion by key (collection order = row order breaks ties)
+      int d = nw++;
+      while (d > 0 && key[(d - 1) * kRBS + tid] > k) {
+        key[d * kRBS + tid] = key[(d - 1) * kRBS + tid];
+        kw[d * kRBS + tid] = kw[(d - 1) * kRBS + tid];
+        kc[d * kRBS + tid] = kc[(d - 1) * kRBS + tid];
+        --d;
+      }
+      key[d * kRBS + tid] = k;
+      kw[d * kRBS + tid] = w;
+      kc[d * kRBS + tid] = (unsigned char)(c0i + u);
+    }
+  }
+  if (!(wb <= G && G < wb + win)) {  // exact weights put the crossing below / above the window
+    Straggler s;
+    s.kk = (int)kk;
+    s.j = (int)j;
+    s.G = G;
+    if (G < wb) { s.lo = 0; s.hi = KL - 1; }
+    else { s.lo = KH; s.hi = ~0ULL; }
+    s.wb = 0.0;
+    unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
+    P.strag[slot] = s;
+    return;
+  }
+  // walk to the crossing
+  double cum = wb, v = 0.0;
+  for (int c = 0; c < nw; ++c) {
+    cum += kw[c * kRBS + tid];
+    if (cum > G) {
+      const unsigned long long k = key[c * kRBS + tid];
+      if (k == kZeroKey) {  // a zero takes the sign of its own row: recompute it
+        const int row = (int)rows[(int)kc[c * kRBS + tid] * NP + prob];
+        v = __ddiv_rn(xcol[row], pr[row].b);
+      } else {
+        v = key64_inv(k);
+      }
+      break;
+    }
+  }
+  // window residual at v from the exact ratios: |x_ij - v x_ip| = |x_ip| |r_i - v|
+  double ew = 0.0;
+  for (int c = 0; c < nw; ++c) ew += kw[c * kRBS + tid] * fabs(key64_inv(key[c * kRBS + tid]) - v);
+  const double wa = Tq - wb - win;  // exact
+  P.V[prob] = v;
+  P.E[prob] = es + ew * unit + (v - c0) * ((wb - wa) * unit);
 }
 
 // Route every problem of a shard to the straggler queue (inputs outside the
@@ -591,6 +706,7 @@ __global__ void k_queue_all(SelParams P) {
   unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
   P.strag[slot] = s;
 }
+
 
 // ----------------------------------------------------------- stragglers --
 //
@@ -624,10 +740,6 @@ __device__ __forceinline__ double sratio(const SelParams& P, double a, double b,
   return b != 0.0 ? __ddiv_rn(a, b) : __longlong_as_double(0x7ff8000000000000LL);
 }
 
-__device__ __forceinline__ double warp_sum(double x) {
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
 
 // Visit every row with nonzero weight of problem (p, j): f(row, key, weight).
 // kSUnroll rows per lane are loaded before any is used, so a warp keeps
