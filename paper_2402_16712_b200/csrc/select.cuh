@@ -102,34 +102,36 @@ __device__ __forceinline__ bool region_G(double Tq, double wneg, double Lsc, dou
   return true;
 }
 
-// smem planes of one staged chunk (kRows rows); a pass stages only the
-// planes it reads.  Shared-memory wavefronts, not arithmetic, bound this
-// kernel, so every staged byte is one a pass actually uses.
-constexpr int kTileF = kRows * 32 * 4;           // a32 tile [row][32 targets]
-constexpr int kTileA = kRows * 32 * 8;           // a (f64) tile
-constexpr int kPlaneF = kWarps * kRows * 8;      // (y32, w32) [row][8 pivots]
-constexpr int kPlaneBW = kWarps * kRows * 16;    // (x_ip, wq) [row][8 pivots]
-constexpr int kRingF = 32 * 1024;                // ring of the F passes
+// Shared memory: [cbuf | ring | histograms].  The F passes stream through
+// cbuf + ring (cbuf is only filled by pass B), pass B through ring +
+// histograms (those are dead by then), so each pass gets the deepest ring
+// the 2-CTA/SM budget allows.  A pass stages only the planes it reads, in
+// chunks of R rows (64 for the plain F pass, 32 otherwise).
+constexpr int kRingMid = 24 * 1024;              // the ring both halves share
 constexpr int kHistBytes = kNB * kBS * 4;        // per-thread histograms [slot][thread]
-constexpr int kRingB = kRingF + kHistBytes;      // pass B also streams through the histogram space
 constexpr int kMaxStages = 8;
 
 template <typename RowT, int CAP>
+__host__ __device__ constexpr int cbuf_bytes() { return (int)(sizeof(RowT) * CAP * kBS); }
+template <typename RowT, int CAP>
 constexpr size_t select_smem() {
-  return (size_t)kRingB + sizeof(RowT) * CAP * kBS;
+  return (size_t)cbuf_bytes<RowT, CAP>() + kRingMid + kHistBytes;
 }
 
 enum : unsigned { W_F = 1, W_A = 2, W_PF = 4, W_BW = 8 };
 
-// Byte offsets of the planes inside one stage for a given plane set.
+// Byte offsets of the planes inside one stage for a given plane set and
+// chunk height R; the ring is [base, base + ring).
 struct StageLayout {
-  int f, a, pf, bw, bytes, nst;
-  __device__ StageLayout(unsigned want, int ring) {
+  int f, a, pf, bw, bytes, nst, R, base;
+  __device__ StageLayout(unsigned want, int rows, int ring_base, int ring) {
+    R = rows;
+    base = ring_base;
     int o = 0;
-    f = o; o += (want & W_F) ? kTileF : 0;
-    a = o; o += (want & W_A) ? kTileA : 0;
-    pf = o; o += (want & W_PF) ? kPlaneF : 0;
-    bw = o; o += (want & W_BW) ? kPlaneBW : 0;
+    f = o; o += (want & W_F) ? R * 32 * 4 : 0;        // a32 tile [row][32 targets]
+    a = o; o += (want & W_A) ? R * 32 * 8 : 0;        // a (f64) tile
+    pf = o; o += (want & W_PF) ? R * kWarps * 8 : 0;  // (y32, w32) [row][8 pivots]
+    bw = o; o += (want & W_BW) ? R * kWarps * 16 : 0; // (x_ip, wq) [row][8 pivots]
     bytes = o;
     nst = min(kMaxStages, ring / o);
   }
@@ -137,10 +139,10 @@ struct StageLayout {
 
 template <typename RowT, int CAP>
 __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
-  static_assert(CAP * 8 <= kNB * 4, "resolve keys live in the histogram space");
   extern __shared__ __align__(128) unsigned char smem[];
-  float* hist = (float*)(smem + kRingF);                                  // [kNB][kBS]
-  RowT* cbuf = (RowT*)(smem + kRingB);                                    // [CAP][kBS]
+  constexpr int kCb = cbuf_bytes<RowT, CAP>();
+  RowT* cbuf = (RowT*)smem;                                               // [CAP][kBS]
+  float* hist = (float*)(smem + kCb + kRingMid);                          // [kNB][kBS]
   __shared__ __align__(8) unsigned long long full[kMaxStages], empty[kMaxStages];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -180,7 +182,6 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   }
   __syncthreads();
   unsigned fphase = 0, ephase = 0, used = 0;  // per-barrier bits
-  const int64_t nch = (n + kRows - 1) / kRows;
   const int64_t tbase = (int64_t)blockIdx.x * np * 32;  // this CTA's target tile
   const int64_t gbase = (int64_t)blockIdx.y * np * 8;   // this CTA's pivot group
   auto issue = [&](const StageLayout& L, int64_t c, unsigned want) {
@@ -192,20 +193,21 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     }
     used |= 1u << st;
     if (lane == 0) {
-      const int64_t i0 = c * kRows;
-      unsigned char* base = smem + (size_t)st * L.bytes;
+      const int64_t i0 = c * L.R;
+      unsigned char* base = smem + L.base + (size_t)st * L.bytes;
       fence_proxy_async();
       mbar_expect_tx(&full[st], (unsigned)L.bytes);
-      if (want & W_F) bulk_g2s(base + L.f, P.Xft + tbase + i0 * 32, kTileF, &full[st]);
-      if (want & W_A) bulk_g2s(base + L.a, P.Xt + tbase + i0 * 32, kTileA, &full[st]);
-      if (want & W_PF) bulk_g2s(base + L.pf, P.gpf + gbase + i0 * 8, kPlaneF, &full[st]);
-      if (want & W_BW) bulk_g2s(base + L.bw, P.gbw + gbase + i0 * 8, kPlaneBW, &full[st]);
+      if (want & W_F) bulk_g2s(base + L.f, P.Xft + tbase + i0 * 32, L.R * 32 * 4, &full[st]);
+      if (want & W_A) bulk_g2s(base + L.a, P.Xt + tbase + i0 * 32, L.R * 32 * 8, &full[st]);
+      if (want & W_PF) bulk_g2s(base + L.pf, P.gpf + gbase + i0 * 8, L.R * kWarps * 8, &full[st]);
+      if (want & W_BW) bulk_g2s(base + L.bw, P.gbw + gbase + i0 * 8, L.R * kWarps * 16, &full[st]);
     }
     __syncwarp();
   };
-  // body(stage base, layout, rows, first_row) on every chunk
-  auto sweep = [&](unsigned want, int ring, bool busy, auto&& body) {
-    const StageLayout L(want, ring);
+  // body(stage base, layout, rows, first_row) on every chunk of R rows
+  auto sweep = [&](unsigned want, int rows, int ring_base, int ring, bool busy, auto&& body) {
+    const StageLayout L(want, rows, ring_base, ring);
+    const int64_t nch = (n + rows - 1) / rows;
     fence_proxy_async();  // generic writes to the ring space (histograms) before async copies
     __syncthreads();      // every stage of the previous pass has been consumed
     for (int64_t c = 0; c < min((int64_t)(L.nst - 1), nch); ++c) issue(L, c, want);
@@ -214,12 +216,14 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       const int st = (int)(c % L.nst);
       mbar_wait(&full[st], (fphase >> st) & 1u);
       fphase ^= 1u << st;
-      if (busy) body((const unsigned char*)smem + (size_t)st * L.bytes, L, (int)min((int64_t)kRows, n - c * kRows),
-                     c * kRows);
+      if (busy) body((const unsigned char*)smem + L.base + (size_t)st * L.bytes, L,
+                     (int)min((int64_t)rows, n - c * rows), c * rows);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   };
+  constexpr int kRingFB = 0, kRingFS = kCb + kRingMid;              // F passes: cbuf + ring
+  constexpr int kRingBB = kCb, kRingBS = kRingMid + kHistBytes;     // pass B: ring + histograms
   auto tF = [&](const unsigned char* b, const StageLayout& L) { return (const float*)(b + L.f); };
   auto tA = [&](const unsigned char* b, const StageLayout& L) { return (const double*)(b + L.a); };
   // plane entries of row r for this warp's pivot: [r * 8 + warp]
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     for (int b = 0; b < kNB; ++b) hist[b * kBS + tid] = 0.f;
     const unsigned hbase = smem_u32(hist + tid) - 0x4B000000u * (unsigned)(kBS * 4);
     const bool busy = __any_sync(0xffffffffu, live);
-    // One F pass over a staged chunk, all kRows rows (pad rows past n have
+    // One F pass over a staged chunk, all R rows (pad rows past n have
     // y = w = wq = 0 and add nothing).  Rows go in batches of 4: the tile and
     // plane loads and slot arithmetic of a batch are issued first, then the
     // four histogram read-modify-writes, whose program order (volatile asm)
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       const float2* pf = pF(sb, L);
       const double2* bw = pBW(sb, L);
 #pragma unroll 2
-      for (int r0 = 0; r0 < kRows; r0 += 4) {
+      for (int r0 = 0; r0 < L.R; r0 += 4) {
         float2 yw[4];
         float av[4];
         double wq[4];
@@ -348,21 +352,14 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
           const float uu = __saturatef(fmaf(q[u], A, B));
           addr[u] = hbase + __float_as_uint(fmaf(uu, 63.f, 8388608.f)) * (unsigned)(kBS * 4);
         }
-        // the four slot reads go out together; a row whose slot an earlier
-        // row of the batch also hit adds that row's weight too, and the
-        // stores go in row order, so the last store to a slot carries every
-        // update -- no read waits for a store
-        float h[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h[u]) : "r"(addr[u]));
+        // read-modify-writes in row order (volatile asm keeps same-slot
+        // updates ordered); the loads and slot arithmetic above are not
+        // part of the serial chain
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          float t = h[u] + yw[u].y;
-#pragma unroll
-          for (int v = 0; v < u; ++v)
-            asm("{\n .reg .pred e;\n setp.eq.u32 e, %1, %2;\n @e add.f32 %0, %0, %3;\n}"
-                : "+f"(t) : "r"(addr[u]), "r"(addr[v]), "f"(yw[v].y));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(t));
+          float h;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h) : "r"(addr[u]));
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(h + yw[u].y));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -374,7 +371,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     };
     double base;
     if (!exact_f) {  // single float pass (pass == 0)
-      sweep(W_F | W_PF, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+      sweep(W_F | W_PF, 64, kRingFB, kRingFS, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
         fbody(sb, L, std::integral_constant<int, 0>{});
       });
       float T32 = 0.f;
@@ -387,13 +384,13 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       if (fabsf(D32) + 1e-7f * (float)n * T32 < lam32 * (1.f - 1e-6f)) live = false;
       base = (double)hist[tid];
     } else if (pass == 0) {
-      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+      sweep(W_F | W_PF | W_BW, 32, kRingFB, kRingFS, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
         fbody(sb, L, std::integral_constant<int, 1>{});
       });
       if (live && !region_G(Tq, wneg, Lsc, &G)) live = false;  // dead column
       base = wlow * unit;
     } else {
-      sweep(W_F | W_PF | W_BW, kRingF, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
+      sweep(W_F | W_PF | W_BW, 32, kRingFB, kRingFS, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
         fbody(sb, L, std::integral_constant<int, 2>{});
       });
       base = wlow * unit;
@@ -467,7 +464,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     // batches of 4 rows: loads first, then the (branch-free) bookkeeping;
     // pad rows past n (all zeros) add nothing and are never collected
 #pragma unroll 2
-    for (int r0 = 0; r0 < kRows; r0 += 4) {
+    for (int r0 = 0; r0 < L.R; r0 += 4) {
       float q32[4];
       double2 bw[4];
       double a[4];
@@ -496,11 +493,13 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   };
   const bool busyB = __any_sync(0xffffffffu, live);
   if (exact_f)
-    sweep(W_F | W_A | W_PF | W_BW, kRingB, busyB, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
+    sweep(W_F | W_A | W_PF | W_BW, 32, kRingBB, kRingBS, busyB,
+          [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
       bbody(sb, L, rmax, i0, std::false_type{});
     });
   else
-    sweep(W_F | W_A | W_PF | W_BW, kRingB, busyB, [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
+    sweep(W_F | W_A | W_PF | W_BW, 32, kRingBB, kRingBS, busyB,
+          [&](const unsigned char* sb, const StageLayout& L, int rmax, int64_t i0) {
       bbody(sb, L, rmax, i0, std::true_type{});
     });
   __syncthreads();  // the ring (incl. the histogram space) is free for the resolve keys
@@ -576,17 +575,28 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
 
 constexpr int kRBS = 128;  // threads per k_resolve block
 
+constexpr int kNSB = 16;  // exact-weight sub-bins of the window in k_resolve
+constexpr int kList = 8;  // rows of the crossing sub-bin ordered exactly
+
 template <typename RowT, int CAP>
 constexpr size_t resolve_smem() {
-  return (size_t)kRBS * CAP * (2 * sizeof(double) + 1);
+  return (size_t)kRBS * (kNSB * 2 * sizeof(double) + kList * (2 * sizeof(double) + 1));
 }
 
+// Thread per problem; work linear in the window size (no sort of the whole
+// window): (1a) exact keys of the collected rows, guard-band rows settled,
+// the window rows' exact weights (and weighted offsets, for the residual)
+// summed into 16 sub-bins that split [Lw, Hw) monotonically in the exact
+// ratio; the walk finds the crossing sub-bin; (1b) the rows of that sub-bin
+// (usually one or two) are re-gathered and ordered exactly by (key, row).
 template <typename RowT, int CAP>
 __global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
   extern __shared__ __align__(16) unsigned char rsm[];
-  unsigned long long* key = (unsigned long long*)rsm;             // [CAP][kRBS]
-  double* kw = (double*)(rsm + (size_t)kRBS * CAP * 8);           // [CAP][kRBS] weight
-  unsigned char* kc = rsm + (size_t)kRBS * CAP * 16;              // [CAP][kRBS] collection index
+  double* sbW = (double*)rsm;                                         // [kNSB][kRBS]
+  double* sbR = sbW + kNSB * kRBS;                                    // [kNSB][kRBS]
+  unsigned long long* lk = (unsigned long long*)(sbR + kNSB * kRBS);  // [kList][kRBS]
+  double* lw = (double*)(lk + kList * kRBS);                          // [kList][kRBS]
+  unsigned char* lc = (unsigned char*)(lw + kList * kRBS);            // [kList][kRBS]
   const int tid = threadIdx.x;
   const int64_t NP = P.npiv * P.m;
   const int64_t prob = (int64_t)blockIdx.x * kRBS + tid;
@@ -600,80 +610,136 @@ __global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
   double wb = P.rwb[prob], es = P.res[prob];
   const double c0 = Lw > -kBig ? Lw : Hw;
   const double Tq = P.tq[p];
-  const double unit = ldexp(1.0, -P.spow[p]);
+  const int sp = P.spow[p];
+  const double unit = ldexp(1.0, -sp);
   const double* xcol = P.Xc + j * n;
-  const PRec* pr = P.prec + p * P.np;
+  const double* pbp = P.pb + p * P.np;
   const RowT* rows = (const RowT*)P.rrows;
   const unsigned long long KL = key64(Lw), KH = key64(Hw);
-  double win = 0.0;
-  // phase 1: exact keys (two L2 sectors per row: x_ij and the pivot record),
-  // four rows in flight; guard-band rows outside [Lw, Hw) and dropped rows
-  // are settled here, the window rows kept as (key, weight)
-  int nw = 0;
-  for (int c0i = 0; c0i < cnt; c0i += 4) {
-    double a[4];
-    double2 by[4], wz[4];
+  // sub-bin s <-> exact ratio r in [Lw + s/scale, Lw + (s+1)/scale); an open
+  // window (an infinite edge) puts every row in sub-bin 0
+  const double span = Hw - Lw;
+  const bool finite = span > 0.0 && span < 1e300;
+  const double scale = finite ? (double)kNSB / span : 0.0;
+  const double width = finite ? span * (1.0 / kNSB) : 0.0;
+  auto subbin = [&](double r) { return min(kNSB - 1, max(0, (int)((r - Lw) * scale))); };
+  // reference point of a sub-bin for the weighted offsets (any fixed value
+  // near the sub-bin works; it only keeps the sums small)
+  auto edge = [&](int sb) { return finite ? __fma_rn((double)sb, width, Lw) : 0.0; };
+  for (int sb = 0; sb < kNSB; ++sb) {
+    sbW[sb * kRBS + tid] = 0.0;
+    sbR[sb * kRBS + tid] = 0.0;
+  }
+  // exact key and weight of collected row c (x_ij, x_ip gathered -- L2
+  // resident; the pivot's reciprocal and weight recomputed as K0 did)
+  auto gather4 = [&](int c0i, double* a, double* bb) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const bool ok = c0i + u < cnt;
       const int row = ok ? (int)rows[(c0i + u) * NP + prob] : 0;
       a[u] = ok ? xcol[row] : 0.0;
-      by[u] = ok ? reinterpret_cast<const double2*>(pr + row)[0] : make_double2(0.0, 0.0);
-      wz[u] = ok ? reinterpret_cast<const double2*>(pr + row)[1] : make_double2(0.0, 0.0);
+      bb[u] = ok ? pbp[row] : 0.0;
     }
+  };
+  double win = 0.0;
+  for (int c0i = 0; c0i < cnt; c0i += 4) {  // phase 1a
+    double a[4], bb[4];
+    gather4(c0i, a, bb);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (c0i + u >= cnt) break;
-      const double w = wz[u].x;
-      const unsigned long long k = key64(ratio_fast(a[u], by[u].x, by[u].y));
-      if (w == 0.0) continue;  // dropped row: |x_ij| already in es
+      if (bb[u] == 0.0) continue;  // dropped row: no weight, |x_ij| already in es
+      const double w = rint(ldexp(fabs(bb[u]), sp));
+      const double q = ratio_fast(a[u], bb[u], recip_refined(bb[u]));
+      const unsigned long long k = key64(q);
       if (k < KL) { wb += w; continue; }
       if (k >= KH) continue;
-      es -= fabs(__fma_rn(-by[u].x, c0, a[u]));  // pass B added every row
+      es -= fabs(__fma_rn(-bb[u], c0, a[u]));  // pass B added every row
       win += w;
-      // stable insertion by key (collection order = row order breaks ties)
-      int d = nw++;
-      while (d > 0 && key[(d - 1) * kRBS + tid] > k) {
-        key[d * kRBS + tid] = key[(d - 1) * kRBS + tid];
-        kw[d * kRBS + tid] = kw[(d - 1) * kRBS + tid];
-        kc[d * kRBS + tid] = kc[(d - 1) * kRBS + tid];
-        --d;
-      }
-      key[d * kRBS + tid] = k;
-      kw[d * kRBS + tid] = w;
-      kc[d * kRBS + tid] = (unsigned char)(c0i + u);
+      const int sb = subbin(q);
+      sbW[sb * kRBS + tid] += w;
+      sbR[sb * kRBS + tid] += w * (q - edge(sb));
     }
   }
-  if (!(wb <= G && G < wb + win)) {  // exact weights put the crossing below / above the window
+  bool ok = wb <= G && G < wb + win;
+  int sstar = 0;
+  double cum = wb;
+  if (ok) {
+    for (sstar = 0; sstar < kNSB - 1; ++sstar) {
+      const double h = sbW[sstar * kRBS + tid];
+      if (cum + h > G) break;
+      cum += h;
+    }
+  }
+  // phase 1b: the crossing sub-bin's rows, ordered exactly (stable insertion;
+  // collection order is row order)
+  int nl = 0;
+  if (ok) {
+    for (int c0i = 0; c0i < cnt && nl <= kList; c0i += 4) {
+      double a[4], bb[4];
+      gather4(c0i, a, bb);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (c0i + u >= cnt || bb[u] == 0.0) continue;
+        const double q = ratio_fast(a[u], bb[u], recip_refined(bb[u]));
+        const unsigned long long k = key64(q);
+        if (k < KL || k >= KH || subbin(q) != sstar) continue;
+        if (nl == kList) { nl = kList + 1; break; }
+        int d = nl++;
+        while (d > 0 && lk[(d - 1) * kRBS + tid] > k) {
+          lk[d * kRBS + tid] = lk[(d - 1) * kRBS + tid];
+          lw[d * kRBS + tid] = lw[(d - 1) * kRBS + tid];
+          lc[d * kRBS + tid] = lc[(d - 1) * kRBS + tid];
+          --d;
+        }
+        lk[d * kRBS + tid] = k;
+        lw[d * kRBS + tid] = rint(ldexp(fabs(bb[u]), sp));
+        lc[d * kRBS + tid] = (unsigned char)(c0i + u);
+      }
+    }
+    ok = nl <= kList;  // heavy ties inside one sub-bin: the straggler solver takes it
+  }
+  double v = 0.0;
+  if (ok) {
+    ok = false;
+    for (int c = 0; c < nl; ++c) {
+      cum += lw[c * kRBS + tid];
+      if (cum > G) {
+        const unsigned long long k = lk[c * kRBS + tid];
+        if (k == kZeroKey) {  // a zero takes the sign of its own row
+          const int row = (int)rows[(int)lc[c * kRBS + tid] * NP + prob];
+          v = __ddiv_rn(xcol[row], pbp[row]);
+        } else {
+          v = key64_inv(k);
+        }
+        ok = true;
+        break;
+      }
+    }
+  }
+  if (!ok) {
     Straggler s;
     s.kk = (int)kk;
     s.j = (int)j;
     s.G = G;
-    if (G < wb) { s.lo = 0; s.hi = KL - 1; }
-    else { s.lo = KH; s.hi = ~0ULL; }
+    if (G < wb) { s.lo = 0; s.hi = KL - 1; }               // crossing below the window
+    else if (G >= wb + win) { s.lo = KH; s.hi = ~0ULL; }   // above it
+    else { s.lo = KL; s.hi = KH - 1; }                     // inside, heavy ties
     s.wb = 0.0;
     unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
     P.strag[slot] = s;
     return;
   }
-  // walk to the crossing
-  double cum = wb, v = 0.0;
-  for (int c = 0; c < nw; ++c) {
-    cum += kw[c * kRBS + tid];
-    if (cum > G) {
-      const unsigned long long k = key[c * kRBS + tid];
-      if (k == kZeroKey) {  // a zero takes the sign of its own row: recompute it
-        const int row = (int)rows[(int)kc[c * kRBS + tid] * NP + prob];
-        v = __ddiv_rn(xcol[row], pr[row].b);
-      } else {
-        v = key64_inv(k);
-      }
-      break;
-    }
-  }
-  // window residual at v from the exact ratios: |x_ij - v x_ip| = |x_ip| |r_i - v|
+  // window residual at v: whole sub-bins below / above v from their sums
+  // (sum w (v - r) = W (v - edge) - R, sum w (r - v) = R + W (edge - v)),
+  // the crossing sub-bin's rows one by one (|x_ij - v x_ip| = |x_ip||r - v|)
   double ew = 0.0;
-  for (int c = 0; c < nw; ++c) ew += kw[c * kRBS + tid] * fabs(key64_inv(key[c * kRBS + tid]) - v);
+  for (int sb = 0; sb < kNSB; ++sb) {
+    const double W = sbW[sb * kRBS + tid], R = sbR[sb * kRBS + tid];
+    if (sb < sstar) ew += W * (v - edge(sb)) - R;
+    else if (sb > sstar) ew += R + W * (edge(sb) - v);
+  }
+  for (int c = 0; c < nl; ++c) ew += lw[c * kRBS + tid] * fabs(key64_inv(lk[c * kRBS + tid]) - v);
   const double wa = Tq - wb - win;  // exact
   P.V[prob] = v;
   P.E[prob] = es + ew * unit + (v - c0) * ((wb - wa) * unit);
