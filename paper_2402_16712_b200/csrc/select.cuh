@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
   const double Tq = P.tq[p];
   const int sp = P.spow[p];
   const double unit = ldexp(1.0, -sp);
+  const double scale2 = ldexp(1.0, sp);  // |x_ip| * 2^s is exact: a power-of-two product
   const double* xcol = P.Xc + j * n;
   const double* pbp = P.pb + p * P.np;
   const RowT* rows = (const RowT*)P.rrows;
@@ -649,7 +650,7 @@ __global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
     for (int u = 0; u < 4; ++u) {
       if (c0i + u >= cnt) break;
       if (bb[u] == 0.0) continue;  // dropped row: no weight, |x_ij| already in es
-      const double w = rint(ldexp(fabs(bb[u]), sp));
+      const double w = rint(fabs(bb[u]) * scale2);
       const double q = ratio_fast(a[u], bb[u], recip_refined(bb[u]));
       const unsigned long long k = key64(q);
       if (k < KL) { wb += w; continue; }
@@ -693,7 +694,7 @@ __global__ void __launch_bounds__(kRBS) k_resolve(SelParams P) {
           --d;
         }
         lk[d * kRBS + tid] = k;
-        lw[d * kRBS + tid] = rint(ldexp(fabs(bb[u]), sp));
+        lw[d * kRBS + tid] = rint(fabs(bb[u]) * scale2);
         lc[d * kRBS + tid] = (unsigned char)(c0i + u);
       }
     }
