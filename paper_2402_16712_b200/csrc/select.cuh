@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     // keeps same-slot updates correct -- so only the RMWs, not the loads,
     // form the serial chain.  KIND 0: float single pass (+ float Wneg);
     // 1: exact first pass (+ exact Wneg and slot-0 weight); 2: exact later
-    // pass (+ slot-0 weight).
+    // pass (+ slot-0 weight); 3: float single pass for a lambda far below one
+    // bin's weight, where G = T/2 up to << a bin and no Wneg is needed.
     float wn32 = 0.f;
     double wlow = 0.0;
     auto fbody = [&](const unsigned char* sb, const StageLayout& L, auto kind) {
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
         for (int u = 0; u < 4; ++u) {
           yw[u] = pf[(r0 + u) * 8];
           av[u] = ta[(r0 + u) * 32 + lane];
-          if (K != 0) wq[u] = bw[(r0 + u) * 8].y;
+          if (K == 1 || K == 2) wq[u] = bw[(r0 + u) * 8].y;
         }
         unsigned addr[4];
         float q[4];
@@ -363,25 +364,33 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (K == 0 && q[u] < 0.f) wn32 += yw[u].y;
+          if (K == 0 && q[u] < 0.f) wn32 += yw[u].y;  // K 3: lambda too small to move G (no Wneg needed)
           if (K == 1) padd(wneg, wq[u], q[u] < 0.f);                     // exact: signs of q32 are exact
-          if (K != 0) padd(wlow, wq[u], addr[u] == hbase + 0x4B000000u * (unsigned)(kBS * 4));  // slot 0
+          if (K == 1 || K == 2) padd(wlow, wq[u], addr[u] == hbase + 0x4B000000u * (unsigned)(kBS * 4));  // slot 0
         }
       }
     };
     double base;
     if (!exact_f) {  // single float pass (pass == 0)
+      // warp-uniform (one pivot per warp): lambda below 1e-4 of the pivot's
+      // total weight shifts G by far less than a bin holds
+      const bool tiny_lam = P.lam <= 1e-4 * Tq * unit;
       sweep(W_F | W_PF, 64, kRingFB, kRingFS, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
-        fbody(sb, L, std::integral_constant<int, 0>{});
+        if (tiny_lam) fbody(sb, L, std::integral_constant<int, 3>{});
+        else fbody(sb, L, std::integral_constant<int, 0>{});
       });
       float T32 = 0.f;
 #pragma unroll
       for (int b = 0; b < kNB; ++b) T32 += hist[b * kBS + tid];
       const float lam32 = (float)P.lam;
-      const float D32 = T32 - 2.f * wn32;
-      G32 = 0.5f * (T32 - (D32 < -lam32 ? -lam32 : (D32 >= lam32 ? lam32 : 0.f)));
-      // certainly dead (float error of D32 is far below the slack): skip pass B
-      if (fabsf(D32) + 1e-7f * (float)n * T32 < lam32 * (1.f - 1e-6f)) live = false;
+      if (tiny_lam) {
+        G32 = 0.5f * T32;  // pass B decides the region (and deadness) exactly
+      } else {
+        const float D32 = T32 - 2.f * wn32;
+        G32 = 0.5f * (T32 - (D32 < -lam32 ? -lam32 : (D32 >= lam32 ? lam32 : 0.f)));
+        // certainly dead (float error of D32 is far below the slack): skip pass B
+        if (fabsf(D32) + 1e-7f * (float)n * T32 < lam32 * (1.f - 1e-6f)) live = false;
+      }
       base = (double)hist[tid];
     } else if (pass == 0) {
       sweep(W_F | W_PF | W_BW, 32, kRingFB, kRingFS, busy, [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
