@@ -36,7 +36,7 @@
 
 constexpr int kNB = 64;            // F-pass histogram slots: 0 below, 1..62, 63 above
 constexpr int kNI = kNB - 2;       // interior bins
-constexpr int kDelta = 6;          // +- sample ranks around the estimated crossing
+constexpr int kDelta = 7;          // +- sample ranks around the estimated crossing
 constexpr float kGuard = 0x1p-19f; // relative guard band of the float ratios
 constexpr double kBig = 1.7976931348623157e308;  // DBL_MAX: open window side
 
