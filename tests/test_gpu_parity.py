@@ -189,7 +189,9 @@ def _grid(X, bits=20):
     return np.round(X * 2.0**bits) / 2.0**bits
 
 
-@pytest.mark.parametrize("n,m,seed", [(400, 48, 0), (3000, 24, 1), (1, 6, 2), (7, 2, 3), (1000, 33, 4)])
+@pytest.mark.parametrize("n,m,seed", [(400, 48, 0), (3000, 24, 1), (1, 6, 2), (7, 2, 3), (1000, 33, 4),
+                                      (6000, 16, 5),     # two selection passes (n > 4096)
+                                      (70000, 10, 6)])   # three passes, 32-bit row indices (n > 65535)
 def test_grid_data_bit_exact_vs_oracle(n, m, seed):
     d, _ = l1b.gen_line_data(m, n, seed=seed, noise_scale=1.0)
     X = _grid(d.values)
