@@ -107,6 +107,14 @@ int l1b_fit_stats(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t w
  * d_buf must hold 8 * (number of CTAs) uint64.  NULL switches it off. */
 int l1b_set_probe(uint64_t* d_buf);
 
+/* Diagnostics (no reference counterpart): copies up to max_records of the
+ * last l1b_fit_pivots' straggler queue (40-byte records: int32 pivot index
+ * in the shard, int32 target, uint64 key interval lo, hi, double unused,
+ * double G) to host memory; returns the number copied or a status < 0.
+ * Synchronises the stream. */
+int l1b_straggler_records(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes, void* h_out,
+                          int64_t max_records, void* stream);
+
 /* Cumulative count of kernels this library has enqueued in the process
  * (benchmark evidence for "gpu_launches"; no reference counterpart). */
 uint64_t l1b_kernel_launches(void);

@@ -30,6 +30,7 @@ ABI_SYMBOLS = (
     "l1b_dfma_probe",
     "l1b_fit_stats",
     "l1b_set_probe",
+    "l1b_straggler_records",
 )
 
 L1B_OK = 0
@@ -89,6 +90,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_dfma_probe.argtypes = [_i64, _i32, _i32, _vp, _vp]
     lib.l1b_fit_stats.restype = ctypes.c_int
     lib.l1b_fit_stats.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _vp]
+    lib.l1b_straggler_records.restype = ctypes.c_int
+    lib.l1b_straggler_records.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _i64, _vp]
     lib.l1b_set_probe.restype = ctypes.c_int
     lib.l1b_set_probe.argtypes = [_vp]
     _lib = lib

@@ -19,6 +19,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--lam", type=float, default=1.0)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--strag", action="store_true", help="classify the straggler queue")
 a = ap.parse_args()
 shapes = {"c1": (50, 200), "c2": (2000, 2000), "c4": (500, 100000), "c5": (10000, 10000)}
 m, n = shapes[a.config]
@@ -43,3 +44,19 @@ if a.time:
         ev1.synchronize()
         ts.append(ev0.elapsed_time(ev1))
     print("fit_pivots ms", sorted(ts))
+
+if a.strag:
+    import ctypes
+    from paper_2402_16712_b200 import _lib
+    eng.fit_pivots([a.lam], want_v=False)
+    dt = np.dtype([("kk", "<i4"), ("j", "<i4"), ("lo", "<u8"), ("hi", "<u8"), ("wb", "<f8"), ("G", "<f8")])
+    buf = np.zeros(200000, dtype=dt)
+    k = _lib.load().l1b_straggler_records(eng.n, eng.m, eng.max_pivots, eng.ws.data_ptr(), eng.ws.numel(),
+                                          buf.ctypes.data, buf.size, torch.cuda.current_stream().cuda_stream)
+    r = buf[:k]
+    ZERO = 1 << 63
+    lo_open = r["lo"] == 0
+    hi_open = r["hi"] == np.uint64(2**64 - 1)
+    span = (r["hi"].astype(np.float64) - r["lo"].astype(np.float64))
+    print(f"stragglers {k}: lo-open {lo_open.sum()}, hi-open {hi_open.sum()}, finite {(~lo_open & ~hi_open).sum()}; "
+          f"finite-span log2 quantiles {np.percentile(np.log2(span[~lo_open & ~hi_open] + 1), [10, 50, 90]) if (~lo_open & ~hi_open).any() else None}")
