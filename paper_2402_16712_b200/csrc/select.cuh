@@ -107,7 +107,7 @@ __device__ __forceinline__ bool region_G(double Tq, double wneg, double Lsc, dou
 // histograms (those are dead by then), so each pass gets the deepest ring
 // the 2-CTA/SM budget allows.  A pass stages only the planes it reads, in
 // chunks of R rows (64 for the plain F pass, 32 otherwise).
-constexpr int kRingMid = 24 * 1024;              // the ring both halves share
+constexpr int kRingMid = 16 * 1024;              // the ring both halves share
 constexpr int kHistBytes = kNB * kBS * 4;        // per-thread histograms [slot][thread]
 constexpr int kMaxStages = 8;
 
