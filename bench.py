@@ -220,10 +220,25 @@ def run_ours(args):
     from paper_2402_16712_b200.engine import DeviceFit, shard
 
     world, rank, local = _dist_env()
+    # one process per GPU over NCCL; L1B200_DIST_BACKEND=gloo lets several
+    # ranks share a GPU (plumbing check only: the ranks never wait on one
+    # another's kernels, only on host-side collectives)
+    backend = os.environ.get("L1B200_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     lib = _lib.load()
     X, lams = _make_data(args.config)
     n, m = X.shape
@@ -272,11 +287,7 @@ def run_ours(args):
             times.append(ms)
     barrier()
     launches = (lib.l1b_kernel_launches() - launches0) / args.steps
-    ms_local = float(np.sum(times))
-    tot = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms_total = float(tot.item())
+    ms_total = max_over_ranks(float(np.sum(times)))
     solves_step = m * (m - 1) * len(lams) * ncomp
     value = solves_step * args.steps / (ms_total / 1e3)
 
@@ -325,10 +336,7 @@ def run_ours(args):
         if k >= args.warmup:
             e2e_ms.append(ms)
     lines = list(res.components) if ncomp > 1 else res
-    t = torch.tensor([float(np.sum(e2e_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_val = solves_step * args.steps / (float(t.item()) / 1e3)
+    e2e_val = solves_step * args.steps / (max_over_ranks(float(np.sum(e2e_ms))) / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
