@@ -68,6 +68,22 @@ int l1b_fit_pivots(const double* d_X, int64_t n, int64_t m, const double* h_lams
                    int64_t p_begin, int64_t p_stride, int64_t npiv, double* d_V, double* d_err,
                    double* d_pen, double* d_obj, void* d_ws, size_t ws_bytes, void* stream);
 
+/* l1b_fit_pivots for an arbitrary pivot list h_pivots[0..npiv) (host
+ * memory): outputs are indexed by list position.  Used to fit exactly only
+ * the pivots l1b_bound_pivots could not rule out. */
+int l1b_fit_pivot_list(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam,
+                       const int64_t* h_pivots, int64_t npiv, double* d_V, double* d_err, double* d_pen,
+                       double* d_obj, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Pivot pruning for fit_line (fit.py:88-102 needs only the argmin): for
+ * the pivots p_begin + k*p_stride and one lam, one FP32 pass per (pivot,
+ * target) problem yields rigorous bounds d_lb[k] <= z_p <= d_ub[k] on the
+ * pivot objective z_p (error + lam * penalty, core.py:126-133), float error
+ * included as explicit margins.  A pivot with lb > min(ub) cannot be the
+ * winner.  Inputs outside the FP32 window get lb = -inf, ub = +inf. */
+int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
+                     int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
+
 /* Reduction half of fit.py:98-102: per lambda, the strict '<' argmin of
  * d_obj[l][0..npiv) in ascending pivot order (ties -> smallest pivot).
  * Writes d_best_k[l] (index into the shard) and d_best_obj[l]. */

@@ -21,6 +21,8 @@ ABI_SYMBOLS = (
     "l1b_workspace_bytes",
     "l1b_prepare",
     "l1b_fit_pivots",
+    "l1b_fit_pivot_list",
+    "l1b_bound_pivots",
     "l1b_argmin",
     "l1b_residual_exact",
     "l1b_deflate",
@@ -74,6 +76,11 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_pivots.restype = ctypes.c_int
     lib.l1b_fit_pivots.argtypes = [_vp, _i64, _i64, ctypes.POINTER(ctypes.c_double), _i32,
                                    _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_fit_pivot_list.restype = ctypes.c_int
+    lib.l1b_fit_pivot_list.argtypes = [_vp, _i64, _i64, ctypes.POINTER(ctypes.c_double), _i32,
+                                       ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_pivots.restype = ctypes.c_int
+    lib.l1b_bound_pivots.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_argmin.restype = ctypes.c_int
     lib.l1b_argmin.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp]
     lib.l1b_residual_exact.restype = ctypes.c_int

@@ -33,6 +33,10 @@ RESCORE_RTOL = 1e-8
 # residual terms differ by a few ulps of |x_ij| + |v_j x_ip|, so a near-zero
 # objective (an exact fit) needs an absolute floor, not only a relative one
 RESCORE_ATOL = 1e-13
+# pruning keeps every pivot whose lower bound is within this of the best
+# upper bound (the bounds already carry their float-error margins; this
+# covers the reference's own rounding of the objective)
+PRUNE_RTOL = 1e-9
 
 
 def _stream_handle(stream: torch.cuda.Stream | None) -> int:
@@ -81,6 +85,7 @@ class DeviceFit:
         self.X = Xd
         self.n, self.m = int(Xd.shape[0]), int(Xd.shape[1])
         self.max_pivots = self.m if max_pivots is None else int(max_pivots)
+        self.last_candidates = None
         nbytes = self.lib.l1b_workspace_bytes(self.n, self.m, 1, max(1, self.max_pivots))
         if nbytes == 0:
             raise ValueError(f"bad matrix shape {(self.n, self.m)}")
@@ -154,37 +159,98 @@ class DeviceFit:
             return float(self.scalar.item())
 
     # ------------------------------------------------------------- winners --
+    def fit_pivot_list(self, lams, pivots, want_v: bool = True):
+        """K1+K2 for an explicit pivot list: V [L][k][m], err/pen/obj [L][k] in list order."""
+        lam = np.ascontiguousarray(np.atleast_1d(np.asarray(lams, dtype=np.float64)))
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        k = piv.size
+        if k > self.max_pivots:
+            raise ValueError(f"{k} pivots exceed the workspace for {self.max_pivots}")
+        L = lam.size
+        with torch.cuda.device(self.device):
+            V = torch.empty((L, k, self.m), dtype=torch.float64, device=self.device) if want_v else None
+            err = torch.empty((L, k), dtype=torch.float64, device=self.device)
+            pen = torch.empty_like(err)
+            obj = torch.empty_like(err)
+            rc = self.lib.l1b_fit_pivot_list(
+                self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), L,
+                piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), k, V.data_ptr() if want_v else None,
+                err.data_ptr(), pen.data_ptr(), obj.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+        _lib.check(rc, "l1b_fit_pivot_list")
+        return V, err, pen, obj
+
+    def bound_pivots(self, lam: float, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
+        """Rigorous bounds lb <= z_p <= ub of every shard pivot's objective (host arrays)."""
+        if npiv is None:
+            npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, npiv), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_pivots(self.X.data_ptr(), self.n, self.m, float(lam), p_begin, p_stride, npiv,
+                                           b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                                           self._s)
+            _lib.check(rc, "l1b_bound_pivots")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
+    def _winner(self, lam: float, pivots, V, obj_h) -> PivotWinner:
+        """fit.py:98-102 among fitted pivots: re-score the near-minimal ones
+        with the reference's rounding, first strict minimum wins."""
+        o = obj_h
+        if np.isnan(o).any():
+            # FittedLine's invariant rejects a NaN objective (core.py:120-124):
+            # only lam=inf with an all-zero pivot column produces one.
+            raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
+        best = float(o.min())
+        if math.isinf(best):
+            cand = np.nonzero(o == best)[0][:1]
+        else:
+            cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + RESCORE_ATOL * self._abs_scale() + 1e-300)[0]
+        win = None
+        for k in cand:  # ascending pivot order
+            p = int(pivots[k])
+            v_dev = V[k]
+            e = self.residual_exact(v_dev, p)
+            vh = v_dev.cpu().numpy().copy()
+            pn = float(np.abs(vh).sum())
+            z = e + float(lam) * pn
+            if win is None or z < win.objective:
+                win = PivotWinner(p, float(lam), vh, e, pn, z)
+        return win
+
+    def _abs_scale(self) -> float:
+        if self._scale is None:
+            self._scale = self.absmax() * self.n * self.m
+        return self._scale
+
     def shard_winners(self, lams, p_begin: int = 0, p_stride: int = 1,
-                      npiv: int | None = None) -> list[PivotWinner]:
-        """Exact winner of the shard for every lambda (fit.py:98-102 semantics)."""
+                      npiv: int | None = None, prune: bool = True) -> list[PivotWinner]:
+        """Exact winner of the shard for every lambda (fit.py:98-102 semantics).
+
+        With ``prune`` (default) every pivot is first bounded by one FP32 pass
+        (l1b_bound_pivots) and only the pivots whose lower bound does not
+        exceed the smallest upper bound are fitted exactly -- the others
+        provably cannot win, so the result is the same as fitting all.
+        """
         lam = np.atleast_1d(np.asarray(lams, dtype=np.float64))
-        V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
-        obj_h = obj.cpu().numpy()
+        if npiv is None:
+            npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
+        all_piv = p_begin + p_stride * np.arange(npiv, dtype=np.int64)
         out = []
+        if npiv <= 8:  # bounding costs a pass of its own: not worth it for a handful of pivots
+            prune = False
+        if not prune:
+            V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
+            obj_h = obj.cpu().numpy()
+            return [self._winner(float(lam[l]), all_piv, V[l], obj_h[l]) for l in range(lam.size)]
         for l in range(lam.size):
-            o = obj_h[l]
-            if np.isnan(o).any():
-                # FittedLine's invariant rejects a NaN objective (core.py:120-124):
-                # only lam=inf with an all-zero pivot column produces one.
-                raise ValueError(f"objective nan for lam={lam[l]!r} (zero pivot column at infinite penalty)")
-            best = float(o.min())
-            if math.isinf(best):
-                cand = np.nonzero(o == best)[0][:1]
-            else:
-                if self._scale is None:
-                    self._scale = self.absmax() * self.n * self.m
-                cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + RESCORE_ATOL * self._scale + 1e-300)[0]
-            win = None
-            for k in cand:  # ascending pivot order
-                p = p_begin + int(k) * p_stride
-                v_dev = V[l, k]
-                e = self.residual_exact(v_dev, p)
-                vh = v_dev.cpu().numpy().copy()
-                pn = float(np.abs(vh).sum())
-                z = e + float(lam[l]) * pn
-                if win is None or z < win.objective:
-                    win = PivotWinner(p, float(lam[l]), vh, e, pn, z)
-            out.append(win)
+            lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
+            top = float(np.min(ub))
+            thr = top + PRUNE_RTOL * abs(top) + RESCORE_ATOL * self._abs_scale() if np.isfinite(top) else np.inf
+            keep = np.nonzero(~(lb > thr))[0]  # NaN-safe: keep unless provably worse
+            self.last_candidates = int(keep.size)
+            piv = all_piv[keep]
+            V, err, pen, obj = self.fit_pivot_list([lam[l]], piv, want_v=True)
+            out.append(self._winner(float(lam[l]), piv, V[0], obj.cpu().numpy()[0]))
         return out
 
     def selftest_divide(self, n_pairs: int = 1 << 26, seed: int = 1) -> int:

@@ -324,3 +324,48 @@ def test_use_gpu_patches_reference_bindings():
     finally:
         for k in ("fake_l1line", "fake_l1line.core", "fake_l1line.subspace"):
             sys.modules.pop(k, None)
+
+
+# ---------------------------------------------------- pivot pruning bounds --
+
+def _bounds_hold(X, lam):
+    eng = DeviceFit(X)
+    lb, ub = eng.bound_pivots(lam)
+    _, _, _, O = eng.fit_pivots([lam], want_v=False)
+    o = O.cpu().numpy()[0]
+    tol = 1e-12 * np.abs(o) + OBJ_ATOL * float(np.abs(X).sum())
+    assert np.all(lb <= o + tol), (lam, np.max(lb - o))
+    assert np.all(o <= ub + tol), (lam, np.max(o - ub))
+    return lb, ub, o
+
+
+@pytest.mark.parametrize("lam_kind", ["zero", "small", "mid", "large"])
+def test_bounds_contain_every_pivot_objective(lam_kind):
+    """l1b_bound_pivots: lb <= z_p <= ub for every pivot (C1, grid and ragged data)."""
+    g = load_golden("c1.npz")
+    cases = [g["X"], g["Xq"]]
+    d, _ = l1b.gen_line_data(40, 700, seed=11, noise_scale=1.0)
+    cases.append(d.values)
+    rng = np.random.default_rng(5)
+    Z = np.round(rng.uniform(-10, 10, size=(300, 20)) * 4) / 4
+    Z[rng.random(Z.shape) < 0.3] = 0.0
+    cases.append(Z)
+    for X in cases:
+        T = float(np.abs(X).sum(axis=0).max())
+        lam = {"zero": 0.0, "small": 1.0, "mid": 0.2 * T, "large": 0.9 * T}[lam_kind]
+        _bounds_hold(X, lam)
+
+
+def test_pruned_fit_equals_full_fit():
+    """The pruned fit_line path returns exactly what fitting every pivot returns."""
+    for seed, (m, n) in enumerate([(60, 900), (200, 300), (30, 5000)]):
+        d, _ = l1b.gen_line_data(m, n, seed=seed, noise_scale=1.0)
+        X = d.values
+        T = float(np.abs(X).sum(axis=0).max())
+        lams = [0.0, 1.0, 0.1 * T, 0.5 * T]
+        eng = DeviceFit(X)
+        full = eng.shard_winners(lams, prune=False)
+        pruned = eng.shard_winners(lams, prune=True)
+        for a, b in zip(full, pruned):
+            assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes()
+            assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
