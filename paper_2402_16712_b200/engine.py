@@ -236,8 +236,8 @@ class DeviceFit:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         all_piv = p_begin + p_stride * np.arange(npiv, dtype=np.int64)
         out = []
-        if npiv <= 8:  # bounding costs a pass of its own: not worth it for a handful of pivots
-            prune = False
+        if npiv <= 32 or npiv * self.m * self.n < (1 << 24):
+            prune = False  # bounding costs a pass of its own: not worth it for small fits
         if not prune:
             V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
             obj_h = obj.cpu().numpy()
