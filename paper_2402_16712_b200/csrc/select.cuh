@@ -44,13 +44,13 @@ struct SelParams {
   const double* Xt;      // X in 32-column tiles: ((j/32)*np + i)*32 + j%32
   const float* Xft;      // float copy of Xt
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
-  const float2* gpf;     // shard (float y_ip, float |x_ip|) in 8-pivot groups
+  const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
   const double* Xc;      // column-major m x n
   const PRec* prec;      // [m][np] (x_ip, y_ip, wq_ip) records
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
   const double* pw;      // [m][n] fixed-point weight (exact integer)
-  const float2* pf;      // [m][n] (float y, float |x_ip|)
+  const float2* pf;      // [m][n] (float y, float x_ip)
   const double* tq;
   const int* spow;
   const long long* nnz;
@@ -144,183 +144,7 @@ struct StageLayout {
   }
 };
 
-// ---- bound mode (pivot pruning) ---------------------------------------------
-//
-// fit_line needs only the winning pivot, and most pivots' objectives are far
-// above it.  One FP32 pass per problem bounds the column optimum
-//   f_j* = min_v e_j(v) + lam |v|,   e_j(v) = sum_i |x_ij - v x_ip|
-// from below and above: the pass histograms the ratios over the sample
-// bracket (the F pass of k_select) and also sums e_j at the sample centre c.
-// f_j is convex with subgradient g(v) = W(r < v) - W(r > v) + lam sgn(v), so
-// the histogram gives g between its bin edges e_k (up to the float error of
-// the sums) and f at the edges follows from f(c) by integrating g; the
-// optimum lies between the last edge with g <= 0 and the first with g >= 0.
-// Per pivot, z_p = lam + sum_j f_j* (v_p = 1) lies in [LB_p, UB_p]; a pivot
-// whose LB_p exceeds the smallest UB cannot win, and the exact solver runs
-// only on the rest (the host picks them: l1b_bound_pivots + the pivot-list
-// fit).  Every float error enters the bounds as an explicit margin.
-// Residual reference points per problem and their spacing in bins: more
-// points tighten the bounds a little (3 points: -30 % slack at C2) but cost
-// issue slots in the pass; measured best overall is one.
-constexpr int kNRes = 1;
-constexpr float kResStep = 4.f;
-
-template <typename Sweep, typename TF, typename PF>
-__device__ __forceinline__ void bound_pass(const SelParams& P, unsigned char* smem, float* hist, int tid, int lane,
-                                           int warp, int64_t kk, int64_t p, int64_t j, bool piv_ok, bool degenerate,
-                                           bool active, int64_t n, float lo, float hi, float cen, double Tq,
-                                           double unit, Sweep& sweep, TF& tF, PF& pF) {
-  const float A = (62.f / 63.f) / (hi - lo);
-  const float B = 0.5f / 63.f - lo * A;
-#pragma unroll
-  for (int b = 0; b < kNB; ++b) hist[b * kBS + tid] = 0.f;
-  const unsigned hbase = smem_u32(hist + tid) - 0x4B000000u * (unsigned)(kBS * 4);
-  // e_j is summed at kNRes reference points spread around the estimated
-  // crossing (the bound integrates g from the point nearest the crossing, so
-  // its slack grows with that distance)
-  float cfs[kNRes];
-#pragma unroll
-  for (int t = 0; t < kNRes; ++t)
-    cfs[t] = fminf(fmaxf(cen + (float)(t - kNRes / 2) * kResStep * (hi - lo) / (float)kNI, lo), hi);
-  double ec[kNRes];
-#pragma unroll
-  for (int t = 0; t < kNRes; ++t) ec[t] = 0.0;
-  constexpr int kRingFB = 0;
-  const int ring = (int)(hist - (float*)smem) * 4;  // cbuf + ring, as the F passes use
-  sweep(W_F | W_PF, 64, kRingFB, ring, __any_sync(0xffffffffu, active),
-        [&](const unsigned char* sb, const StageLayout& L, int, int64_t) {
-    const float* ta = tF(sb, L);
-    const float2* pf = pF(sb, L);
-    float racc[kNRes];
-#pragma unroll
-    for (int t = 0; t < kNRes; ++t) racc[t] = 0.f;
-#pragma unroll 2
-    for (int r0 = 0; r0 < L.R; r0 += 4) {
-      float2 yw[4];
-      float av[4];
-      unsigned addr[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        yw[u] = pf[(r0 + u) * 8];
-        av[u] = ta[(r0 + u) * 32 + lane];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float q = av[u] * yw[u].x;
-        const float uu = __saturatef(fmaf(q, A, B));
-        addr[u] = hbase + __float_as_uint(fmaf(uu, 63.f, 8388608.f)) * (unsigned)(kBS * 4);
-        const float bs = copysignf(yw[u].y, yw[u].x);  // x_ip in float (dropped rows: 0, term |a|)
-#pragma unroll
-        for (int t = 0; t < kNRes; ++t) racc[t] += fabsf(fmaf(-cfs[t], bs, av[u]));
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float h;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h) : "r"(addr[u]));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(h + yw[u].y));
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < kNRes; ++t) ec[t] += (double)racc[t];
-  });
-  if (!piv_ok || j >= P.m) return;
-  const int64_t o = kk * P.m + j;
-  if (degenerate || j == p) {
-    const double z = degenerate ? P.colsum[j] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
-    P.LB[o] = z;
-    P.UB[o] = z;
-    return;
-  }
-  const double lam = P.lam;
-  const double T = Tq * unit;  // sum_i |x_ip| (fixed-point exact)
-  const double w = ((double)hi - (double)lo) / (double)kNI;
-  // float error margins: histogram sums (worst case n ulps of T), the
-  // residual terms (2^-22 of |a| + |c b|) and their per-chunk float sums
-  const double dC = (double)n * 0x1p-24 * T;
-  // edges e_k = lo + k w (k = 0..62); C_k = weight with r < e_k = slots 0..k.
-  // Ghi(k) >= g(e_k-), Glo(k) <= g(e_k+).
-  auto edge = [&](int k) { return (double)lo + (double)k * w; };
-  int kL = -1, kR = kNB - 1;
-  {
-    double C = 0.0;
-    for (int k = 0; k <= kNI; ++k) {
-      C += (double)hist[k * kBS + tid];
-      const double e = edge(k);
-      const double ghi = 2.0 * (C + dC) - T + (e > 0.0 ? lam : -lam);
-      const double glo = 2.0 * (C - dC) - T + (e >= 0.0 ? lam : -lam);
-      if (ghi <= 0.0) kL = k;
-      if (kR == kNB - 1 && glo >= 0.0) kR = k;
-    }
-  }
-  // anchor: the reference point nearest the crossing interval
-  double c = (double)cfs[0], ecs = ec[0];
-  {
-    const double mid = 0.5 * (edge(max(kL, 0)) + edge(min(kR, kNI)));
-#pragma unroll
-    for (int t = 1; t < kNRes; ++t)
-      if (fabs((double)cfs[t] - mid) < fabs(c - mid)) { c = (double)cfs[t]; ecs = ec[t]; }
-  }
-  const double eps = 0x1p-22 * (P.colsum[j] + fabs(c) * T) + 64.0 * 0x1p-24 * ecs;
-  const double fc = ecs + lam * fabs(c);
-  // integrals of the per-bin subgradient bounds from e_0: I(k) = sum_{q<k} w g(q)
-  const int kc = min(kNI - 1, max(0, (int)floor((c - (double)lo) / w)));
-  double Ilo = 0.0, Ihi = 0.0, IloC = 0.0, IhiC = 0.0, IloL = 0.0, IhiL = 0.0, IloR = 0.0, IhiR = 0.0;
-  double gloC = 0.0, ghiC = 0.0, gloL = 0.0;
-  {
-    double C = (double)hist[tid];
-    for (int k = 0; k <= kNI; ++k) {
-      if (k == kc) { IloC = Ilo; IhiC = Ihi; }
-      if (k == kL) { IloL = Ilo; IhiL = Ihi; }
-      if (k == kR) { IloR = Ilo; IhiR = Ihi; }
-      if (k == kNI) break;
-      const double Cn = C + (double)hist[(k + 1) * kBS + tid];
-      const double glo = 2.0 * (C - dC) - T + (edge(k) >= 0.0 ? lam : -lam);        // g on [e_k, e_k+1] >=
-      const double ghi = 2.0 * (Cn + dC) - T + (edge(k + 1) > 0.0 ? lam : -lam);    // g on [e_k, e_k+1] <=
-      if (k == kc) { gloC = glo; ghiC = ghi; }
-      if (k == kL) gloL = glo;
-      Ilo += w * glo;
-      Ihi += w * ghi;
-      C = Cn;
-    }
-  }
-  // f at e_kc from f(c), then at any edge k from e_kc
-  const double dc = c - edge(kc);
-  const double fkc_lo = fc - dc * ghiC, fkc_hi = fc - dc * gloC;
-  auto f_lo = [&](int k, double Ilk, double Ihk) { return k >= kc ? fkc_lo + (Ilk - IloC) : fkc_lo - (IhiC - Ihk); };
-  auto f_hi = [&](int k, double Ilk, double Ihk) { return k >= kc ? fkc_hi + (Ihk - IhiC) : fkc_hi - (IloC - Ilk); };
-  // v = 0 is always feasible and f(0) = sum_i |x_ij| exactly (the column's
-  // dead value); the penalty's kink at 0 also gets its own tangent bounds
-  const double f0 = P.colsum[j];
-  double lb, ub = fmin(fc + eps, f0);
-  const double eL = kL >= 0 ? edge(kL) : -INFINITY, eR = kR <= kNI ? edge(kR) : INFINITY;
-  if (kL >= 0 && kR <= kNI && kL <= kR) {
-    lb = f_lo(kL, IloL, IhiL) - eps + fmin(0.0, gloL) * (eR - eL);
-    ub = fmin(ub, fmin(f_hi(kL, IloL, IhiL), f_hi(kR, IloR, IhiR)) + eps);
-  } else {
-    lb = 0.0;  // the optimum lies beyond the bracket: only the trivial bound
-    if (kL == kNI) ub = fmin(ub, f_hi(kNI, Ilo, Ihi) + eps);
-  }
-  if (eL <= 0.0 && 0.0 <= eR) {
-    // g(0-) <= 2 W(r < eR) - T - lam, g(0+) >= 2 W(r < eL) - T + lam
-    double CL = 0.0, CR = 0.0;
-    for (int k = 0; k <= kNI; ++k) {
-      const double h = (double)hist[k * kBS + tid];
-      if (k <= kL) CL += h;
-      if (k <= kR) CR += h;
-    }
-    if (kR > kNI) CR = T;
-    const double g0m = 2.0 * (CR + dC) - T - lam, g0p = 2.0 * (CL - dC) - T + lam;
-    // f(v) >= f0 + g(0-) v on v <= 0, f(v) >= f0 + g(0+) v on v >= 0; both
-    // sides also bounded by the tangent at eL above
-    const double left = isfinite(eL) ? f0 + fmax(0.0, g0m) * eL : (g0m <= 0.0 ? f0 : 0.0);
-    const double right = isfinite(eR) ? f0 + fmin(0.0, g0p) * eR : (g0p >= 0.0 ? f0 : 0.0);
-    lb = fmax(lb, fmin(left, right));
-  }
-  P.LB[o] = fmax(0.0, lb);
-  P.UB[o] = ub;
-}
-
-template <typename RowT, int CAP, bool BOUND>
+template <typename RowT, int CAP>
 __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int kCb = cbuf_bytes<RowT, CAP>();
@@ -419,7 +243,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   };
   stamp(0);
   // ---- sample: float ratios of 32 strided rows, sorted -> value bracket ----
-  float lo = 0.f, hi = 0.f, cen = 0.f;  // bracket and the estimated crossing
+  float lo = 0.f, hi = 0.f;
   if (active) {
     float sr[kSample], sw[kSample];
 #pragma unroll
@@ -427,7 +251,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
       int64_t r = ((2 * s + 1) * n) / (2 * kSample);
       float2 f = P.pf[p * P.np + r];
       sr[s] = P.Xft[tbase + r * 32 + lane] * f.x;
-      sw[s] = f.y;
+      sw[s] = fabsf(f.y);
     }
 #pragma unroll
     for (int k = 2; k <= kSample; k <<= 1) {
@@ -470,7 +294,6 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     for (int s = 0; s < kSample; ++s) {
       if (s == lo_i) lo = sr[s];
       if (s == hi_i) hi = sr[s];
-      if (s == sstar) cen = sr[s];
     }
   }
   if (!(hi > lo)) {  // degenerate sample (or idle lane): a tiny bracket around it
@@ -481,11 +304,6 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
 
   __syncthreads();
   stamp(1);
-  if constexpr (BOUND) {
-    bound_pass(P, smem, hist, tid, lane, warp, kk, p, j, piv_ok, degenerate, active, n, lo, hi, cen, Tq, unit, sweep,
-               tF, pF);
-    return;
-  }
   // ---- F passes: 64-slot FP32 histograms, each narrowing the range ---------
   // slot(r) = RN(63 * sat(r * A + B)): slot 0 <-> r < lo, slot b in 1..62 <->
   // r in [lo + (b-1) w, lo + b w) with w = (hi - lo) / 62, slot 63 <-> r >= hi
@@ -549,11 +367,11 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
         for (int u = 0; u < 4; ++u) {
           float h;
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h) : "r"(addr[u]));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(h + yw[u].y));
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr[u]), "f"(h + fabsf(yw[u].y)));
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          if (K == 0 && q[u] < 0.f) wn32 += yw[u].y;  // K 3: lambda too small to move G (no Wneg needed)
+          if (K == 0 && q[u] < 0.f) wn32 += fabsf(yw[u].y);  // K 3: lambda too small to move G (no Wneg needed)
           if (K == 1) padd(wneg, wq[u], q[u] < 0.f);                     // exact: signs of q32 are exact
           if (K == 1 || K == 2) padd(wlow, wq[u], addr[u] == hbase + 0x4B000000u * (unsigned)(kBS * 4));  // slot 0
         }
