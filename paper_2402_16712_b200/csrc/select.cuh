@@ -46,7 +46,6 @@ struct SelParams {
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
   const double* Xc;      // column-major m x n
-  const PRec* prec;      // [m][np] (x_ip, y_ip, wq_ip) records
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
   const double* pw;      // [m][n] fixed-point weight (exact integer)
