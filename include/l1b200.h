@@ -84,6 +84,16 @@ int l1b_fit_pivot_list(const double* d_X, int64_t n, int64_t m, const double* h_
 int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
                      int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
+/* l1b_bound_pivots for a pivot list (host memory) with 1 to 3 passes per
+ * problem: every further pass re-histograms the bin of the subgradient's
+ * sign change (62 sub-bins; or extends the bracket when the optimum lay
+ * outside it) and the last sums the residual at its centre, which tightens
+ * the bounds by orders of magnitude per pass -- used on the pivots the
+ * one-pass bounds could not rule out. */
+int l1b_bound_pivot_list(const double* d_X, int64_t n, int64_t m, double lam, const int64_t* h_pivots,
+                         int64_t npiv, int32_t passes, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes,
+                         void* stream);
+
 /* Reduction half of fit.py:98-102: per lambda, the strict '<' argmin of
  * d_obj[l][0..npiv) in ascending pivot order (ties -> smallest pivot).
  * Writes d_best_k[l] (index into the shard) and d_best_obj[l]. */
@@ -130,6 +140,24 @@ int l1b_set_probe(uint64_t* d_buf);
  * Synchronises the stream. */
 int l1b_straggler_records(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes, void* h_out,
                           int64_t max_records, void* stream);
+
+/* Exact fit (as l1b_fit_pivot_list, one lambda) of a short pivot list that
+ * a preceding l1b_bound_pivot_list call on this workspace bounded: pivot k
+ * is entry h_seed[k] of that call's list of seed_npiv pivots (-1: no seed).
+ * Every (pivot, target) problem goes to the warp-per-problem exact solver,
+ * started on the range the bound passes left for its optimum (typically a
+ * handful of rows, so one collecting pass), instead of the batched
+ * k_select path whose per-CTA row loop is latency-bound for few pivots.
+ * Results are identical to l1b_fit_pivot_list. */
+int l1b_fit_pivot_list_seeded(const double* d_X, int64_t n, int64_t m, double lam, const int64_t* h_pivots,
+                              int64_t npiv, const int64_t* h_seed, int64_t seed_npiv, double* d_V, double* d_err,
+                              double* d_pen, double* d_obj, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Per-column bounds lb_pj <= f_j* <= ub_pj ([npiv][m], pivot order) of the
+ * last l1b_bound_* call on this workspace, which bounded npiv pivots; copied
+ * to host memory (test and diagnostic accessor).  Synchronises the stream. */
+int l1b_bound_columns(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes, double* h_lb,
+                      double* h_ub, void* stream);
 
 /* Cumulative count of kernels this library has enqueued in the process
  * (benchmark evidence for "gpu_launches"; no reference counterpart). */

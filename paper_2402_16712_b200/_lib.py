@@ -23,6 +23,7 @@ ABI_SYMBOLS = (
     "l1b_fit_pivots",
     "l1b_fit_pivot_list",
     "l1b_bound_pivots",
+    "l1b_bound_pivot_list",
     "l1b_argmin",
     "l1b_residual_exact",
     "l1b_deflate",
@@ -33,6 +34,8 @@ ABI_SYMBOLS = (
     "l1b_fit_stats",
     "l1b_set_probe",
     "l1b_straggler_records",
+    "l1b_bound_columns",
+    "l1b_fit_pivot_list_seeded",
 )
 
 L1B_OK = 0
@@ -81,6 +84,9 @@ def load() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_bound_pivots.restype = ctypes.c_int
     lib.l1b_bound_pivots.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_pivot_list.restype = ctypes.c_int
+    lib.l1b_bound_pivot_list.argtypes = [_vp, _i64, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), _i64,
+                                         _i32, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_argmin.restype = ctypes.c_int
     lib.l1b_argmin.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp]
     lib.l1b_residual_exact.restype = ctypes.c_int
@@ -99,6 +105,11 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_stats.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _vp]
     lib.l1b_straggler_records.restype = ctypes.c_int
     lib.l1b_straggler_records.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _i64, _vp]
+    lib.l1b_bound_columns.restype = ctypes.c_int
+    lib.l1b_bound_columns.argtypes = [_i64, _i64, _i64, _vp, _sz, _vp, _vp, _vp]
+    lib.l1b_fit_pivot_list_seeded.restype = ctypes.c_int
+    lib.l1b_fit_pivot_list_seeded.argtypes = [_vp, _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64, _vp, _vp,
+                                              _vp, _vp, _vp, _sz, _vp]
     lib.l1b_set_probe.restype = ctypes.c_int
     lib.l1b_set_probe.argtypes = [_vp]
     _lib = lib

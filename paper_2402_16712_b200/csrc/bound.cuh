@@ -7,8 +7,10 @@
 //     f_j* = min_v e_j(v) + lam |v|,   e_j(v) = sum_i |x_ij - v x_ip|
 // from below and above:
 //   * the pass histograms the ratios r_i = x_ij / x_ip over the sample bracket
-//     (64 slots: below / 62 bins / above, as k_select's first pass) and sums
-//     e_j at the sample centre c;
+//     (64 slots: below / 62 bins / above, as k_select's first pass; weights
+//     are 32-bit fixed point, wq / 2^21, so the sums are exact and the only
+//     weight error is the rounding of each weight) and sums e_j at the sample
+//     centre c;
 //   * f_j is convex with subgradient g(v) = W(r < v) - W(r > v) + lam sgn(v),
 //     so the histogram bounds g on every bin, f at the bin edges follows from
 //     f(c) by integrating those bounds, and the optimum lies between the last
@@ -26,27 +28,39 @@
 // problems, halving the shared-memory loads per problem, and the two
 // histogram read-modify-write chains interleave.
 
-constexpr int kBWarps = 4;                 // warps per k_bound CTA (2 pivots each)
+constexpr int kBPairs = 4;                 // pivot pairs per k_bound CTA (8 pivots)
+constexpr int kBWarps = 2 * kBPairs;       // two row halves per pair
 constexpr int kBThreads = kBWarps * 32;
+constexpr int kBSlots = kBPairs * 32;      // histogram columns: (pair, target)
 constexpr int kBRows = 64;                 // rows per staged chunk
 constexpr int kBTile = kBRows * 32 * 4;    // x_ij float tile [row][32 targets]
-constexpr int kBPlane = kBRows * kWarps * 8;   // (y32, w32) [row][8 pivots]
-constexpr int kBStage = kBTile + kBPlane;
-constexpr int kBStages = 4;
-constexpr int kBHist = 2 * kNB * kBThreads * 4;  // [problem][slot][thread]
+constexpr int kBPlane = kBRows * kWarps * 8;   // (y32, x_ip32) [row][8 pivots]
+constexpr int kBPlaneU = kBRows * kWarps * 4;  // 32-bit weights [row][8 pivots]
+constexpr int kBStage = kBTile + kBPlane + kBPlaneU;
+constexpr int kBStages = 3;
+constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [problem][bin][slot], exact 32-bit sums
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
+// bracket half-width in sample ranks: narrow for the one-pass bound (tight
+// bins), wider when later passes refine it (fewer optima outside)
+constexpr int kBDelta1 = 7, kBDeltaN = 10;
 
-// Bounds of one column optimum from its histogram h[slot * hs] over the
-// bracket [lo, hi) (62 interior bins), e_j(c) = ec, the exact pivot weight T
-// and the column's sum_i |x_ij| (f(0)).
-__device__ __forceinline__ void column_bounds(const float* h, int hs, double lo, double hi, double c, double ec,
-                                              double T, double lam, double colsum, int64_t n, double* lbo,
-                                              double* ubo) {
+// Bounds of one column optimum from its histogram h[slot * hs] (exact sums
+// of 32-bit weights of q each) over the bracket [lo, hi) (62 interior bins),
+// e_j(c) = ec, the exact pivot weight T and the column's sum_i |x_ij| (f(0)).
+__device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double q, double lo, double hi, double c,
+                                              double ec, double T, double lam, double colsum, int64_t n,
+                                              double* lbo, double* ubo, double2* range) {
   const double w = (hi - lo) / (double)kNI;
-  // float margins: histogram sums (worst case n ulps of T), the residual
-  // terms (2^-22 of |a| + |c b|) and their per-chunk float sums
-  const double dC = (double)n * 0x1p-24 * T;
-  const double eps = 0x1p-22 * (colsum + fabs(c) * T) + 64.0 * 0x1p-24 * ec;
+  // margins: the 32-bit weights are within q/2 of |x_ip| each (so any
+  // cumulative weight within n q / 2), the residual terms within 2^-22 of
+  // |a| + |c b|, and their per-chunk float sums
+  const double dC = 0.5000001 * (double)n * q;
+  // every row's float ratio (and the float bin edges) sit within pert / w_i
+  // of its binned position, so f moves by at most pert when the rows are
+  // moved into their bins; the bounds below hold for that moved problem
+  const double pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
+  // (a chunk sums 16 pairwise 4-row sums: relative error <= 18 u)
+  const double eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
   const double fc = ec + lam * fabs(c);
   // edges e_k = lo + k w (k = 0..62); C_k = weight with r < e_k = slots 0..k
   auto edge = [&](int k) { return lo + (double)k * w; };
@@ -60,7 +74,7 @@ __device__ __forceinline__ void column_bounds(const float* h, int hs, double lo,
   double Ilo = 0.0, Ihi = 0.0, IloC = 0.0, IhiC = 0.0, IloL = 0.0, IhiL = 0.0, IloR = 0.0, IhiR = 0.0;
   double gloC = 0.0, ghiC = 0.0, gloL = 0.0;
   {
-    double C = (double)h[0];
+    double C = (double)h[0] * q;
     double ghiE = 2.0 * (C + dC) - T + (edge(0) > 0.0 ? lam : -lam);
     double gloE = 2.0 * (C - dC) - T + (edge(0) >= 0.0 ? lam : -lam);
     for (int k = 0; k <= kNI; ++k) {
@@ -69,7 +83,7 @@ __device__ __forceinline__ void column_bounds(const float* h, int hs, double lo,
       if (kR == kNB - 1 && gloE >= 0.0) { kR = k; CR = C; IloR = Ilo; IhiR = Ihi; }
       if (k == kc) { IloC = Ilo; IhiC = Ihi; }
       if (k == kNI || (kR < kNB - 1 && k > kc)) break;  // everything needed is captured
-      const double Cn = C + (double)h[(k + 1) * hs];
+      const double Cn = C + (double)h[(k + 1) * hs] * q;
       const double ghiN = 2.0 * (Cn + dC) - T + (edge(k + 1) > 0.0 ? lam : -lam);
       const double gloN = 2.0 * (Cn - dC) - T + (edge(k + 1) >= 0.0 ? lam : -lam);
       // g on [e_k, e_k+1] lies in [gloE, ghiN]
@@ -102,17 +116,26 @@ __device__ __forceinline__ void column_bounds(const float* h, int hs, double lo,
     const double g0m = 2.0 * (CR + dC) - T - lam, g0p = 2.0 * ((kL >= 0 ? CL : 0.0) - dC) - T + lam;
     const double left = isfinite(eL) ? f0 + fmax(0.0, g0m) * eL : (g0m <= 0.0 ? f0 : 0.0);
     const double right = isfinite(eR) ? f0 + fmin(0.0, g0p) * eR : (g0p >= 0.0 ? f0 : 0.0);
-    lb = fmax(lb, fmin(left, right));
+    lb = fmax(lb, fmin(left, right) - pert);
   }
   *lbo = fmax(0.0, lb);
   *ubo = ub;
+  // where the optimum lies (seed for the exact solver), widened for the
+  // rows' float ratios and edges
+  if (kL >= 0 && kR <= kNI && kL <= kR) {
+    const double d = 0x1p-19 * (fabs(eL) + fabs(eR) + fabs(lo) + fabs(hi)) + 0x1p-10 * w;
+    *range = make_double2(eL - d, eR + d);
+  } else {
+    *range = make_double2(-INFINITY, INFINITY);
+  }
 }
 
 // Sample bracket of one problem: float ratios of 32 strided rows, bitonic
 // sorted in registers; returns the bracket +-kDelta ranks around the
 // estimated crossing and that estimate (the residual's reference point).
 __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
-                                               double unit, float* lo, float* hi, float* cen) {
+                                               double unit, int delta, float* lo, float* hi, float* cen,
+                                               float* smin, float* smax) {
   const int64_t n = P.n;
   float sr[kSample], sw[kSample];
 #pragma unroll
@@ -159,7 +182,7 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
     c += sw[s];
     if (!got && c > t) { sstar = s; got = true; }
   }
-  const int lo_i = max(sstar - kDelta, 0), hi_i = min(sstar + kDelta, kSample - 1);
+  const int lo_i = max(sstar - delta, 0), hi_i = min(sstar + delta, kSample - 1);
   float l = 0.f, hh = 0.f, ce = 0.f;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
@@ -175,13 +198,29 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
   *lo = l;
   *hi = hh;
   *cen = fminf(fmaxf(ce, l), hh);
+  *smin = sr[0];
+  *smax = sr[kSample - 1];
 }
 
+// NPASS = 1: one pass over the sample bracket.  NPASS > 1 (refinement for
+// the pivots the first stage could not rule out): every pass but the last
+// only histograms its range; the next re-histograms the range where the
+// optimum provably lies with 62 sub-bins, so the integration error shrinks
+// with the square of the bin width; the last pass also sums e_j at its centre.
+//
+// Threads: warps w and w + 4 own the same pivot pair (2w', 2w'+1, w' = w % 4)
+// and target (lane) and split each chunk's rows (alternate 4-row groups);
+// both add into the problem's one histogram with shared-memory atomics, so
+// the CTA holds 8 warps for the histogram space of 4.
+template <int NPASS>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
-  float* hist = (float*)(smem + kBStages * kBStage);  // [2][kNB][kBThreads]
+  unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
   __shared__ __align__(8) unsigned long long full[kBStages], empty[kBStages];
+  __shared__ float sbr[2][5][kBSlots];  // brackets: problem t's (lo, hi, cen, smin, smax) per slot
+  __shared__ double sec[kBSlots];       // e_j(c) of problem 0 from the other half
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int half = warp / kBPairs, pair = warp % kBPairs, slot = pair * 32 + lane;
   const int64_t n = P.n, m = P.m, np = P.np;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   const int64_t tbase = (int64_t)blockIdx.x * np * 32;  // this CTA's target tile
@@ -190,21 +229,30 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   int64_t kk[2], p[2];
   bool ok[2], degen[2], act[2];
   double Tq[2], unit[2];
-  float lo[2], hi[2], cen[2];
+  float lo[2], hi[2], cen[2], smin[2], smax[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    kk[t] = (int64_t)blockIdx.y * kWarps + 2 * warp + t;
+    kk[t] = (int64_t)blockIdx.y * kWarps + 2 * pair + t;
     ok[t] = kk[t] < P.npiv;
     p[t] = ok[t] ? pivot_of(P, kk[t]) : 0;
     degen[t] = ok[t] && P.nnz[p[t]] == 0;
     act[t] = ok[t] && !degen[t] && j < m && j != p[t];
     Tq[t] = ok[t] && !degen[t] ? P.tq[p[t]] : 0.0;
     unit[t] = ldexp(1.0, ok[t] && !degen[t] ? -P.spow[p[t]] : 0);
-    lo[t] = hi[t] = cen[t] = 0.f;
-    if (act[t]) sample_bracket(P, p[t], tbase, lane, Tq[t], unit[t], &lo[t], &hi[t], &cen[t]);
-    else { lo[t] = -1.f; hi[t] = 1.f; }
   }
-
+  {  // each half samples one problem's bracket; both halves need both
+    const bool h = half != 0;
+    float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
+    if (h ? act[1] : act[0])
+      sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0],
+                     NPASS == 1 ? kBDelta1 : kBDeltaN, &b0, &b1, &b2, &b3, &b4);
+    float* d = &sbr[half][0][slot];
+    d[0] = b0;
+    d[kBSlots] = b1;
+    d[2 * kBSlots] = b2;
+    d[3 * kBSlots] = b3;
+    d[4 * kBSlots] = b4;
+  }
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
       mbar_init(&full[s], 1);
@@ -212,29 +260,27 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     }
     mbar_fence_init();
   }
-  float A[2], B[2], cf[2];
-  unsigned hb[2];
+  __syncthreads();
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    A[t] = (62.f / 63.f) / (hi[t] - lo[t]);
-    B[t] = 0.5f / 63.f - lo[t] * A[t];
-    cf[t] = cen[t];
-#pragma unroll
-    for (int b = 0; b < kNB; ++b) hist[(t * kNB + b) * kBThreads + tid] = 0.f;
-    hb[t] = smem_u32(hist + t * kNB * kBThreads + tid) - 0x4B000000u * (unsigned)(kBThreads * 4);
+    lo[t] = sbr[t][0][slot];
+    hi[t] = sbr[t][1][slot];
+    cen[t] = sbr[t][2][slot];
+    smin[t] = sbr[t][3][slot];
+    smax[t] = sbr[t][4][slot];
   }
-  fence_proxy_async();
-  __syncthreads();
 
   const int64_t nch = (n + kBRows - 1) / kBRows;
-  unsigned ephase = 0;
+  unsigned ephase = 0, fphase = 0;
+  int64_t issued = 0;  // chunks issued over all passes (stage = issued % kBStages)
   auto issue = [&](int64_t c) {
     if (warp != 0) return;
-    const int st = (int)(c % kBStages);
-    if (c >= kBStages) {
+    const int st = (int)(issued % kBStages);
+    if (issued >= kBStages) {
       mbar_wait(&empty[st], (ephase >> st) & 1u);
       ephase ^= 1u << st;
     }
+    ++issued;
     if (lane == 0) {
       const int64_t i0 = c * kBRows;
       unsigned char* base = smem + (size_t)st * kBStage;
@@ -242,74 +288,157 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
       mbar_expect_tx(&full[st], (unsigned)kBStage);
       bulk_g2s(base, P.Xft + tbase + i0 * 32, kBTile, &full[st]);
       bulk_g2s(base + kBTile, P.gpf + gbase + i0 * 8, kBPlane, &full[st]);
+      bulk_g2s(base + kBTile + kBPlane, P.gwu + gbase + i0 * 8, kBPlaneU, &full[st]);
     }
     __syncwarp();
   };
   const bool busy = __any_sync(0xffffffffu, act[0] || act[1]);
-  double ec0 = 0.0, ec1 = 0.0;  // e_j(c) of both problems
-  unsigned fphase = 0;
-  for (int64_t c = 0; c < min((int64_t)(kBStages - 1), nch); ++c) issue(c);
-  for (int64_t c = 0; c < nch; ++c) {
-    if (c + kBStages - 1 < nch) issue(c + kBStages - 1);
-    const int st = (int)(c % kBStages);
-    mbar_wait(&full[st], (fphase >> st) & 1u);
-    fphase ^= 1u << st;
-    if (busy) {
-      const unsigned char* sb = smem + (size_t)st * kBStage;
-      const float* ta = (const float*)sb;
-      const float4* pf4 = (const float4*)(sb + kBTile) + warp;  // (y, x_ip) of pivots 2w, 2w+1
-      float r0acc = 0.f, r1acc = 0.f;
+  int64_t consumed = 0;  // chunks consumed over all passes
+  double ec0 = 0.0, ec1 = 0.0;  // this half's share of e_j(c) of both problems (last pass)
+  float cf[2];
+  for (int pass = 0; pass < NPASS; ++pass) {
+    const bool resid = pass == NPASS - 1;
+    float A[2], B[2];
+    unsigned hb[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      A[t] = (62.f / 63.f) / (hi[t] - lo[t]);
+      B[t] = 0.5f / 63.f - lo[t] * A[t];
+      cf[t] = pass == 0 ? cen[t] : 0.5f * (lo[t] + hi[t]);
+      if (half == t) {
+#pragma unroll
+        for (int b = 0; b < kNB; ++b) hist[(t * kNB + b) * kBSlots + slot] = 0u;
+      }
+      hb[t] = smem_u32(hist + t * kNB * kBSlots + slot) - 0x4B000000u * (unsigned)(kBSlots * 4);
+    }
+    __syncthreads();
+    const int64_t c0 = consumed;
+    for (int64_t c = 0; c < min((int64_t)(kBStages - 1), nch); ++c) issue(c);
+    for (int64_t c = 0; c < nch; ++c) {
+      if (c + kBStages - 1 < nch) issue(c + kBStages - 1);
+      const int st = (int)((c0 + c) % kBStages);
+      mbar_wait(&full[st], (fphase >> st) & 1u);
+      fphase ^= 1u << st;
+      if (busy) {
+        const unsigned char* sb = smem + (size_t)st * kBStage;
+        const float* ta = (const float*)sb;
+        const float4* pf4 = (const float4*)(sb + kBTile) + pair;  // (y, x_ip) of pivots 2w', 2w'+1
+        const uint2* pu2 = (const uint2*)(sb + kBTile + kBPlane) + pair;  // their 32-bit weights
+        float r0acc = 0.f, r1acc = 0.f;
 #pragma unroll 2
-      for (int r0 = 0; r0 < kBRows; r0 += 4) {
-        float av[4];
-        float4 yw[4];
+        for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
+          float av[4];
+          float4 yw[4];
+          uint2 wu[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          av[u] = ta[(r0 + u) * 32 + lane];
-          yw[u] = pf4[(r0 + u) * 4];
+          for (int u = 0; u < 4; ++u) {
+            av[u] = ta[(r0 + u) * 32 + lane];
+            yw[u] = pf4[(r0 + u) * 4];
+            wu[u] = pu2[(r0 + u) * 4];
+          }
+          unsigned a0[4], a1[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float q0 = av[u] * yw[u].x, q1 = av[u] * yw[u].z;
+            a0[u] = hb[0] + __float_as_uint(fmaf(__saturatef(fmaf(q0, A[0], B[0])), 63.f, 8388608.f)) *
+                                (unsigned)(kBSlots * 4);
+            a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
+                                (unsigned)(kBSlots * 4);
+          }
+          if (resid) {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
+            float e0[4], e1[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              e0[u] = fabsf(fmaf(-cf[0], yw[u].y, av[u]));
+              e1[u] = fabsf(fmaf(-cf[1], yw[u].w, av[u]));
+            }
+            r0acc += (e0[0] + e0[1]) + (e0[2] + e0[3]);
+            r1acc += (e1[0] + e1[1]) + (e1[2] + e1[3]);
+          }
+          // fire-and-forget shared adds (the other half adds into the same bins)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[u]), "r"(wu[u].x));
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[u]), "r"(wu[u].y));
+          }
         }
-        unsigned a0[4], a1[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float q0 = av[u] * yw[u].x, q1 = av[u] * yw[u].z;
-          a0[u] = hb[0] + __float_as_uint(fmaf(__saturatef(fmaf(q0, A[0], B[0])), 63.f, 8388608.f)) *
-                              (unsigned)(kBThreads * 4);
-          a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
-                              (unsigned)(kBThreads * 4);
-          r0acc += fabsf(fmaf(-cf[0], yw[u].y, av[u]));  // |a - c b| (dropped rows: |a|)
-          r1acc += fabsf(fmaf(-cf[1], yw[u].w, av[u]));
-        }
-        // two independent read-modify-write chains, each in row order
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float h0, h1;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h0) : "r"(a0[u]));
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(h1) : "r"(a1[u]));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a0[u]), "f"(h0 + fabsf(yw[u].y)));
-          asm volatile("st.shared.f32 [%0], %1;" ::"r"(a1[u]), "f"(h1 + fabsf(yw[u].w)));
+        if (resid) {
+          ec0 += (double)r0acc;
+          ec1 += (double)r1acc;
         }
       }
-      ec0 += (double)r0acc;
-      ec1 += (double)r1acc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-  if (j >= m) return;
+    consumed += nch;
+    __syncthreads();  // both halves' adds are in
+    if (pass + 1 < NPASS) {
+      // next range: the edges between which the optimum provably lies (last
+      // edge with g <= 0, first with g >= 0, histogram margins included, as
+      // column_bounds uses them), a little wider; when one side is not in
+      // the bracket the optimum lies beyond it and the range extends there.
+      // Both halves compute it (same inputs, same result).
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    if (!ok[t]) continue;
-    const int64_t o = kk[t] * m + j;
-    if (degen[t] || j == p[t]) {
-      const double z = degen[t] ? P.colsum[j] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
-      P.LB[o] = z;
-      P.UB[o] = z;
-      continue;
+      for (int t = 0; t < 2; ++t) {
+        if (!act[t]) continue;
+        const double T = Tq[t] * unit[t], lam = P.lam, w = ((double)hi[t] - (double)lo[t]) / (double)kNI;
+        const double q = ldexp(unit[t], 21), dC = 0.5000001 * (double)n * q;
+        double C = 0.0;
+        int kL = -1, kR = -1;
+        for (int k = 0; k <= kNI; ++k) {
+          C += (double)hist[(t * kNB + k) * kBSlots + slot] * q;
+          const double e = (double)lo[t] + (double)k * w;
+          if (2.0 * (C + dC) - T + (e > 0.0 ? lam : -lam) <= 0.0) kL = k;
+          if (2.0 * (C - dC) - T + (e >= 0.0 ? lam : -lam) >= 0.0) { kR = k; break; }
+        }
+        const float span = hi[t] - lo[t];
+        float a, b;
+        if (kL >= 0 && kR >= 0) {
+          a = (float)((double)lo[t] + (double)max(0, min(kL, kR - 1)) * w);
+          b = (float)((double)lo[t] + (double)min(kNI, max(kR, kL + 1)) * w);
+        } else if (kR >= 0) {  // optimum at or below lo: extend down
+          a = fminf(smin[t], lo[t]) - 2.f * span;
+          b = (float)((double)lo[t] + (double)kR * w);
+        } else if (kL >= 0) {  // at or above the last edge: extend up
+          a = (float)((double)lo[t] + (double)kL * w);
+          b = fmaxf(smax[t], hi[t]) + 2.f * span;
+        } else {  // no edge is decisive (margins dominate): keep the range
+          a = lo[t];
+          b = hi[t];
+        }
+        const float mg = 0.05f * (b - a);
+        lo[t] = a - mg;
+        hi[t] = b + mg;
+        if (!(hi[t] > lo[t])) hi[t] = lo[t] + fmaxf(fabsf(lo[t]), 1e-30f) * 1e-6f;
+      }
+      __syncthreads();  // histograms read before the next pass clears them
     }
-    double lb, ub;
-    column_bounds(hist + t * kNB * kBThreads + tid, kBThreads, (double)lo[t], (double)hi[t], (double)cf[t],
-                  t == 0 ? ec0 : ec1, Tq[t] * unit[t], P.lam, P.colsum[j], n, &lb, &ub);
-    P.LB[o] = lb;
-    P.UB[o] = ub;
   }
+  // half 1 finishes problem 1 with half 0's share of its residual, half 0
+  // problem 0 with half 1's share
+  if (half == 1) sec[slot] = ec0;
+  __syncthreads();
+  const double ec = half == 0 ? ec0 + sec[slot] : 0.0;
+  __syncthreads();
+  if (half == 0) sec[slot] = ec1;
+  __syncthreads();
+  const bool h = half != 0;
+  const double ect = h ? ec1 + sec[slot] : ec;
+  if (j >= m || !(h ? ok[1] : ok[0])) return;
+  const int64_t o = (h ? kk[1] : kk[0]) * m + j;
+  const bool dg = h ? degen[1] : degen[0];
+  if (dg || j == (h ? p[1] : p[0])) {
+    const double z = dg ? P.colsum[j] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
+    P.LB[o] = z;
+    P.UB[o] = z;
+    P.BRK[o] = make_double2(-INFINITY, INFINITY);
+    return;
+  }
+  const double ut = h ? unit[1] : unit[0];
+  double lb, ub;
+  column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
+                (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam,
+                P.colsum[j], n, &lb, &ub, &P.BRK[o]);
+  P.LB[o] = lb;
+  P.UB[o] = ub;
 }

@@ -45,6 +45,7 @@ struct SelParams {
   const float* Xft;      // float copy of Xt
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
+  const unsigned* gwu;   // shard wq_ip / 2^21 (rounded) in 8-pivot groups
   const double* Xc;      // column-major m x n
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
@@ -75,6 +76,8 @@ struct SelParams {
   unsigned char* rrows;  // RowT [CAP][npiv*m]
   double* LB;            // bound mode: [npiv][m] lower / upper bound of each column's optimum
   double* UB;
+  double2* BRK;          // bound mode: [npiv][m] range holding each column's optimum v
+  const int64_t* seeds;  // seeded fit: row of BRK (bound-call pivot position) per pivot, -1 none
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {
@@ -785,6 +788,16 @@ __global__ void k_queue_all(SelParams P) {
   s.lo = 0;
   s.hi = ~0ULL;
   s.wb = 0.0;
+  const int64_t sr = P.seeds ? P.seeds[kk] : -1;
+  if (sr >= 0) {
+    // seeded: the bound passes' range for v, widened by a few float ulps;
+    // a range that misses is widened by k_straggle itself
+    const double2 r = P.BRK[sr * P.m + j];
+    if (r.x > -INFINITY && r.y < INFINITY && r.x <= r.y) {
+      s.lo = key64(r.x - fabs(r.x) * 0x1p-18 - 0x1p-1000);
+      s.hi = key64(r.y + fabs(r.y) * 0x1p-18 + 0x1p-1000);
+    }
+  }
   unsigned long long slot = atomicAdd(P.nstrag, 1ULL);
   P.strag[slot] = s;
 }
@@ -872,7 +885,9 @@ __global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
     double G = s.G;
     unsigned long long lo = s.lo, hi = s.hi;
     bool dead = false;
-    if (G < 0.0) {  // exact Wneg and key range first
+    // G unknown with a seeded range: the first collecting pass sums Wneg too
+    bool needG = G < 0.0 && !(lo == 0 && hi == ~0ULL);
+    if (G < 0.0 && !needG) {  // exact Wneg and key range first
       double wneg = 0.0;
       unsigned long long kmin = ~0ULL, kmax = 0;
       for_rows<SAFE>(P, p, j, lane, [&](bool ok, int, unsigned long long k, double w) {
@@ -930,9 +945,11 @@ __global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
       }
       // collect the interval's elements (in row order) if they fit
       int base = 0;
+      double wneg = 0.0;
       for_rows<SAFE>(P, p, j, lane, [&](bool okr, int row, unsigned long long k, double w) {
         const bool in = okr && k >= lo && k <= hi;
         if (okr && k < lo) wbl += w;
+        if (needG && okr && k < kZeroKey) wneg += w;
         const unsigned mask = __ballot_sync(0xffffffffu, in);
         const int pos = base + __popc(mask & ((1u << lane) - 1));
         if (in && pos < kSCap) ent[warp][pos] = SEnt{k, w, row, 0};
@@ -940,6 +957,14 @@ __global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
       });
       wbl = warp_sum(wbl);
       __syncwarp();
+      if (needG) {
+        needG = false;
+        if (!region_G(Tq, warp_sum(wneg), Lsc, &G)) {  // dead: v = 0
+          v = 0.0;
+          ok = true;
+          break;
+        }
+      }
       if (G < wbl) {  // the crossing lies below the interval
         hi = lo - 1;
         lo = 0;

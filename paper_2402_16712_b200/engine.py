@@ -37,6 +37,11 @@ RESCORE_ATOL = 1e-13
 # upper bound (the bounds already carry their float-error margins; this
 # covers the reference's own rounding of the objective)
 PRUNE_RTOL = 1e-9
+# refine (multi-pass bounds on the survivors) when the one-pass bounds keep
+# more than this many pivots; three passes cost ~3 one-pass bounds per pivot
+# (a quarter of an exact fit or less) and leave one or a few candidates
+REFINE_MIN = 2
+REFINE_PASSES = 3
 
 
 def _stream_handle(stream: torch.cuda.Stream | None) -> int:
@@ -179,6 +184,24 @@ class DeviceFit:
         _lib.check(rc, "l1b_fit_pivot_list")
         return V, err, pen, obj
 
+    def fit_pivot_list_seeded(self, lam: float, pivots, seed, seed_npiv: int):
+        """fit_pivot_list for one lambda, seeded by the last bound call (l1b_fit_pivot_list_seeded):
+        pivot k was entry seed[k] of that call's list of seed_npiv pivots."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        sd = np.ascontiguousarray(np.asarray(seed, dtype=np.int64))
+        k = piv.size
+        with torch.cuda.device(self.device):
+            V = torch.empty((1, k, self.m), dtype=torch.float64, device=self.device)
+            err = torch.empty((1, k), dtype=torch.float64, device=self.device)
+            pen = torch.empty_like(err)
+            obj = torch.empty_like(err)
+            rc = self.lib.l1b_fit_pivot_list_seeded(
+                self.X.data_ptr(), self.n, self.m, float(lam), piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                k, sd.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(seed_npiv), V.data_ptr(), err.data_ptr(),
+                pen.data_ptr(), obj.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+        _lib.check(rc, "l1b_fit_pivot_list_seeded")
+        return V, err, pen, obj
+
     def bound_pivots(self, lam: float, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
         """Rigorous bounds lb <= z_p <= ub of every shard pivot's objective (host arrays)."""
         if npiv is None:
@@ -191,6 +214,29 @@ class DeviceFit:
             _lib.check(rc, "l1b_bound_pivots")
             bh = b.cpu().numpy()
         return bh[0], bh[1]
+
+    def bound_pivot_list(self, lam: float, pivots, passes: int = REFINE_PASSES):
+        """Bounds for an explicit pivot list; passes 2-3 refine the optimum's range."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, piv.size), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_pivot_list(self.X.data_ptr(), self.n, self.m, float(lam),
+                                               piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), piv.size,
+                                               int(passes), b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(),
+                                               self.ws.numel(), self._s)
+            _lib.check(rc, "l1b_bound_pivot_list")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
+    def bound_columns(self, count: int):
+        """Per-column bounds [count][m] of the last bound call over ``count`` pivots (diagnostics, tests)."""
+        lb = np.empty((count, self.m), dtype=np.float64)
+        ub = np.empty_like(lb)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_bound_columns(self.n, self.m, count, self.ws.data_ptr(), self.ws.numel(),
+                                                  lb.ctypes.data, ub.ctypes.data, self._s),
+                       "l1b_bound_columns")
+        return lb, ub
 
     def _winner(self, lam: float, pivots, V, obj_h) -> PivotWinner:
         """fit.py:98-102 among fitted pivots: re-score the near-minimal ones
@@ -223,10 +269,11 @@ class DeviceFit:
         return self._scale
 
     def shard_winners(self, lams, p_begin: int = 0, p_stride: int = 1,
-                      npiv: int | None = None, prune: bool = True) -> list[PivotWinner]:
+                      npiv: int | None = None, prune: bool | None = None) -> list[PivotWinner]:
         """Exact winner of the shard for every lambda (fit.py:98-102 semantics).
 
-        With ``prune`` (default) every pivot is first bounded by one FP32 pass
+        With ``prune`` (None: when the fit is large enough to pay for it)
+        every pivot is first bounded by one FP32 pass
         (l1b_bound_pivots) and only the pivots whose lower bound does not
         exceed the smallest upper bound are fitted exactly -- the others
         provably cannot win, so the result is the same as fitting all.
@@ -236,8 +283,8 @@ class DeviceFit:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         all_piv = p_begin + p_stride * np.arange(npiv, dtype=np.int64)
         out = []
-        if npiv <= 32 or npiv * self.m * self.n < (1 << 24):
-            prune = False  # bounding costs a pass of its own: not worth it for small fits
+        if prune is None:  # auto: bounding costs a pass of its own, not worth it for small fits
+            prune = npiv > 32 and npiv * self.m * self.n >= (1 << 24)
         if not prune:
             V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
             obj_h = obj.cpu().numpy()
@@ -245,13 +292,27 @@ class DeviceFit:
         for l in range(lam.size):
             lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
             top = float(np.min(ub))
-            thr = top + PRUNE_RTOL * abs(top) + RESCORE_ATOL * self._abs_scale() if np.isfinite(top) else np.inf
-            keep = np.nonzero(~(lb > thr))[0]  # NaN-safe: keep unless provably worse
+            keep = np.nonzero(~(lb > self._prune_threshold(top)))[0]  # NaN-safe: keep unless provably worse
+            seed, seed_n = keep, npiv  # positions in the last bound call's pivot list
+            if keep.size > REFINE_MIN:
+                # second stage on the survivors: every further pass
+                # re-histograms the range holding the optimum, so the bounds
+                # tighten by orders of magnitude; cheaper than exact fits
+                lb2, ub2 = self.bound_pivot_list(float(lam[l]), all_piv[keep], passes=REFINE_PASSES)
+                top = min(top, float(np.min(ub2)))
+                sel = np.nonzero(~(lb2 > self._prune_threshold(top)))[0]
+                keep, seed, seed_n = keep[sel], sel, keep.size
             self.last_candidates = int(keep.size)
             piv = all_piv[keep]
-            V, err, pen, obj = self.fit_pivot_list([lam[l]], piv, want_v=True)
+            # exact fits of the candidates, started on the ranges the bounds left
+            V, err, pen, obj = self.fit_pivot_list_seeded(float(lam[l]), piv, seed, seed_n)
             out.append(self._winner(float(lam[l]), piv, V[0], obj.cpu().numpy()[0]))
         return out
+
+    def _prune_threshold(self, top: float) -> float:
+        if not np.isfinite(top):
+            return np.inf
+        return top + PRUNE_RTOL * abs(top) + RESCORE_ATOL * self._abs_scale()
 
     def selftest_divide(self, n_pairs: int = 1 << 26, seed: int = 1) -> int:
         with torch.cuda.device(self.device):

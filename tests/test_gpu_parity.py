@@ -336,6 +336,31 @@ def _bounds_hold(X, lam):
     tol = 1e-12 * np.abs(o) + OBJ_ATOL * float(np.abs(X).sum())
     assert np.all(lb <= o + tol), (lam, np.max(lb - o))
     assert np.all(o <= ub + tol), (lam, np.max(o - ub))
+    # per column: lb_pj <= f_pj* <= ub_pj with f_pj* from the exact directions
+    V, _, _, _ = eng.fit_pivots([lam], want_v=True)
+    V = V.cpu().numpy()[0]
+    F = np.abs(X[None, :, :] - X.T[:, :, None] * V[:, None, :]).sum(axis=1) + lam * np.abs(V)
+    F[np.arange(X.shape[1]), np.arange(X.shape[1])] = 0.0  # the pivot's own column: v = 1, no error
+    ftol = 1e-12 * F + OBJ_ATOL * float(np.abs(X).sum())
+    cols = bool(np.all(np.isfinite(lb)))  # outside the FP32 window nothing is bounded per column
+    if cols:
+        lbc, ubc = eng.bound_columns(X.shape[1])
+        np.fill_diagonal(lbc, 0.0)
+        np.fill_diagonal(ubc, 0.0)
+        assert np.all(lbc <= F + ftol) and np.all(F <= ubc + ftol), lam
+    # the multi-pass refinement on a pivot list (every other pivot, reversed)
+    piv = np.arange(X.shape[1])[::-2].copy()
+    for passes in (2, 3):
+        lb2, ub2 = eng.bound_pivot_list(lam, piv, passes=passes)
+        assert np.all(lb2 <= o[piv] + tol[piv]), (lam, passes, np.max(lb2 - o[piv]))
+        assert np.all(o[piv] <= ub2 + tol[piv]), (lam, passes, np.max(o[piv] - ub2))
+        if not cols:
+            continue
+        lbc, ubc = eng.bound_columns(piv.size)
+        Fp = F[piv]
+        for k, p in enumerate(piv):
+            lbc[k, p] = ubc[k, p] = 0.0
+        assert np.all(lbc <= Fp + ftol[piv]) and np.all(Fp <= ubc + ftol[piv]), (lam, passes)
     return lb, ub, o
 
 
@@ -365,7 +390,32 @@ def test_pruned_fit_equals_full_fit():
         lams = [0.0, 1.0, 0.1 * T, 0.5 * T]
         eng = DeviceFit(X)
         full = eng.shard_winners(lams, prune=False)
-        pruned = eng.shard_winners(lams, prune=True)
+        pruned = eng.shard_winners(lams, prune=True)  # forced: these sizes are below the auto threshold
         for a, b in zip(full, pruned):
             assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes()
             assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
+
+
+@pytest.mark.parametrize("m,n", [(300, 2000), (40, 70000)])
+def test_seeded_exact_fit_equals_batched_fit(m, n):
+    """l1b_fit_pivot_list_seeded (warp-per-problem solver started on the bound
+    ranges) returns bit-identical V (err / obj to 1e-12) to the batched exact path, for
+    seeds from one-pass and three-pass bounds, and for stale seeds (ranges of
+    other problems: the solver must widen them itself)."""
+    d, _ = l1b.gen_line_data(m, n, seed=3, noise_scale=1.0)
+    X = d.values
+    T = float(np.abs(X).sum(axis=0).max())
+    eng = DeviceFit(X)
+    for lam in (0.0, 1.0, 0.3 * T):
+        piv = np.arange(0, m, 7)
+        V0, e0, _, o0 = eng.fit_pivot_list([lam], piv)
+        V0, e0, o0 = V0.cpu().numpy(), e0.cpu().numpy(), o0.cpu().numpy()
+        for passes in (1, 3):
+            eng.bound_pivot_list(lam, piv, passes=passes)
+            for seed in (np.arange(piv.size), np.arange(piv.size)[::-1].copy()):
+                V1, e1, _, o1 = eng.fit_pivot_list_seeded(lam, piv, seed, piv.size)
+                assert V1.cpu().numpy().tobytes() == V0.tobytes(), (lam, passes)
+                # device error sums differ in summation order between the paths (the winner is re-scored
+                # in NumPy order either way)
+                np.testing.assert_allclose(e1.cpu().numpy(), e0, rtol=1e-12)
+                np.testing.assert_allclose(o1.cpu().numpy(), o0, rtol=1e-12)
