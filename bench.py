@@ -33,6 +33,7 @@ broadcast; total work is fixed, so scaling is "strong".
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -216,7 +217,7 @@ def run_ours(args):
 
     import paper_2402_16712_b200 as l1b
     from paper_2402_16712_b200 import _lib
-    from paper_2402_16712_b200.distributed import combine_winners
+    from paper_2402_16712_b200.distributed import combine_winners, ub_exchange
     from paper_2402_16712_b200.engine import DeviceFit, shard
 
     world, rank, local = _dist_env()
@@ -250,6 +251,9 @@ def run_ours(args):
     eng = DeviceFit(X, device=dev, max_pivots=max(1, npiv))
     X0 = eng.X.clone() if ncomp > 1 else None
 
+    # sharded pruning: one all-reduce(MIN) of the best upper bound per lambda
+    ex = ub_exchange() if world > 1 and eng.auto_prune() else None
+
     def step():
         """One workload pass with X resident: fit_line (every lambda), or
         fit_subspace's fit -> deflate loop (subspace.py:54-76) for C4."""
@@ -261,7 +265,7 @@ def run_ours(args):
         for t in range(ncomp):
             if ncomp > 1 and eng.absmax() <= 1e-10 * scale:
                 break
-            wins = eng.shard_winners(lams, p_begin, p_stride, npiv)
+            wins = eng.shard_winners(lams, p_begin, p_stride, npiv, ub_exchange=ex)
             if world > 1:
                 wins = combine_winners(wins, m)
             out.append(wins)
@@ -302,13 +306,18 @@ def run_ours(args):
         sel_ms.append(ms)
     sel_ms = float(np.median(sel_ms))
     strag = eng.straggler_counts(npiv)[0]
-    # the pruned step's dominant kernel: the bounding pass over every problem
-    bnd_ms = []
+    # the pruned step's dominant kernel: k_bound<1>, the bounding pass over
+    # every problem, timed by the library's CUDA events on its stream
+    bnd_ms, kb_ms = [], []
     for _ in range(max(3, min(args.steps, 5))):
         flush.fill_(1)
         ms, _ = _sync_time(stream, lambda: eng.bound_pivots(lams[0], p_begin, p_stride, npiv))
         bnd_ms.append(ms)
+        kb = ctypes.c_float()
+        _lib.check(lib.l1b_last_bound_ms(ctypes.byref(kb)), "l1b_last_bound_ms")
+        kb_ms.append(kb.value)
     bnd_ms = float(np.median(bnd_ms))
+    kb_ms = float(np.median(kb_ms))
     cand = [None] * len(lams)
     for li, lam_l in enumerate(lams):
         eng.shard_winners([lam_l], p_begin, p_stride, npiv)
@@ -325,6 +334,16 @@ def run_ours(args):
 
     elems = npiv * (m - 1) * n * len(lams)  # ratio elements one fit_pivots call covers on this rank
     achieved = 11.0 * elems / (sel_ms / 1e3)
+
+    # ---- shared-memory atomic peak probe (k_bound's binding operation) -----
+    pu = torch.zeros(1, dtype=torch.int32, device=dev)
+    a_iters, a_blocks, a_thr = 1 << 13, nsm * 2, 256
+    _lib.check(lib.l1b_atoms_probe(a_iters, a_blocks, a_thr, pu.data_ptr(), stream.cuda_stream), "atoms")
+    ams, _ = _sync_time(stream, lambda: _lib.check(
+        lib.l1b_atoms_probe(a_iters, a_blocks, a_thr, pu.data_ptr(), stream.cuda_stream), "atoms"))
+    atoms_peak = 8.0 * a_iters * a_blocks * a_thr / (ams / 1e3)  # lane atomics per second
+    kb_elems = npiv * (m - 1) * n  # one histogram add per (pivot, target, row) per launch
+    kb_rate = kb_elems / (kb_ms / 1e3)
 
     # ---- end to end through the public API (host numpy in, FittedLine out) --
     data = l1b.DataMatrix(X)  # built once, as the reference CLI does before timing fit_line
@@ -368,20 +387,31 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(X.nbytes),
                     "d2h_bytes_per_step": int(8 * m * len(lams) * ncomp + 8 * npiv * len(lams) * ncomp)},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": "k_select+k_resolve+k_straggle (exact fit of every pivot)",
-                         "achieved": achieved / 1e12,
-                         "peak": fp64_ops / 1e12, "unit": "TOP/s (FP64 pipe ops)",
-                         "frac": achieved / fp64_ops, "traffic": None,
-                         "kernel_ms": sel_ms, "ops_per_element": 11, "elements_per_launch": elems,
-                         "stragglers_per_launch": strag,
-                         "peak_source": "measured: l1b_dfma_probe (DFMA/s, 1 op per DFMA)",
-                         "hbm_view": {"algorithmic_bytes": int(8 * n * m), "achieved_GBs": 8 * n * m / (sel_ms / 1e3) / 1e9,
-                                      "peak_GBs": _peak_hbm()}},
+            "roofline": {"bound": "smem_atomic", "kernel": "k_bound<1> (one FP32 bounding pass over every "
+                                                          "(pivot, target, row) element)",
+                         "achieved": kb_rate / 1e9, "peak": atoms_peak / 1e9,
+                         "unit": "G shared-memory atomics/s (one per element)",
+                         "frac": kb_rate / atoms_peak,
+                         "traffic": _ncu_traffic(args.config, world),
+                         "kernel_ms": kb_ms, "elements_per_launch": kb_elems,
+                         "share_of_step": kb_ms * len(lams) * ncomp / (ms_total / args.steps),
+                         "peak_source": "measured: l1b_atoms_probe (conflict-free red.shared.add.u32, "
+                                        "8 in flight per thread)",
+                         "fp32_view": {"ops_per_element": 5, "achieved_TOPs": 5 * kb_rate / 1e12,
+                                       "peak_TOPs": _fp32_peak(dev) / 1e12},
+                         "exact_fit_view": {
+                             "kernel": "k_select+k_resolve+k_straggle (exact fit of every pivot)",
+                             "achieved": achieved / 1e12, "peak": fp64_ops / 1e12,
+                             "unit": "TOP/s (FP64 pipe ops)", "frac": achieved / fp64_ops,
+                             "kernel_ms": sel_ms, "ops_per_element": 11, "elements_per_launch": elems,
+                             "stragglers_per_launch": strag,
+                             "peak_source": "measured: l1b_dfma_probe (DFMA/s, 1 op per DFMA)"}},
             "pruning": {"note": "fit_line needs only the argmin pivot: every (pivot, target) problem is bounded by "
-                                "one FP32 pass (k_select<bound>), pivots whose lower bound exceeds the best upper "
-                                "bound are provably not the winner and skipped; the rest are fitted exactly. "
-                                "Results are identical to fitting every pivot (tests/test_gpu_parity.py::"
-                                "test_pruned_fit_equals_full_fit).",
+                                "one FP32 pass (k_bound<1>), pivots whose lower bound exceeds the best upper "
+                                "bound are provably not the winner; the survivors get three refining passes "
+                                "(k_bound<3>) and the few left are fitted exactly by the warp-per-problem solver "
+                                "started on the ranges the bounds left. Results are identical to fitting every "
+                                "pivot (tests/test_gpu_parity.py::test_pruned_fit_equals_full_fit).",
                         "pivots_per_rank": npiv, "exactly_fitted_per_lambda": cand[:8],
                         "bound_pass_ms": bnd_ms,
                         "bound_pass_fp64_equiv_frac": 11.0 * npiv * (m - 1) * n / (bnd_ms / 1e3) / fp64_ops},
@@ -392,6 +422,31 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _fp32_peak(dev) -> float:
+    """FP32 pipe instructions/s: SMs x 128 lanes x the SM clock (nominal max)."""
+    import torch
+    props = torch.cuda.get_device_properties(dev)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev.index or 0)
+        mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+    except Exception:  # noqa: BLE001
+        mhz = 1965
+    return props.multi_processor_count * 128 * mhz * 1e6
+
+
+def _ncu_traffic(config: str, world: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_bound<1> launch
+    from the committed ncu --set full capture (profiles/r01), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t.get(config) if world == 1 else None
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def _peak_hbm():

@@ -159,6 +159,16 @@ int l1b_fit_pivot_list_seeded(const double* d_X, int64_t n, int64_t m, double la
 int l1b_bound_columns(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes, double* h_lb,
                       double* h_ub, void* stream);
 
+/* Device time (CUDA events on the launching stream) of the last k_bound
+ * launch made by l1b_bound_pivots / l1b_bound_pivot_list; waits for it.
+ * Benchmark evidence for the roofline (no reference counterpart). */
+int l1b_last_bound_ms(float* ms);
+
+/* Shared-memory atomic throughput probe: blocks x threads threads issue
+ * 8 * iters conflict-free 32-bit shared-memory adds each (the operation
+ * k_bound's histograms are built from); bench.py times it for the peak. */
+int l1b_atoms_probe(int64_t iters, int32_t blocks, int32_t threads, uint32_t* d_out, void* stream);
+
 /* Cumulative count of kernels this library has enqueued in the process
  * (benchmark evidence for "gpu_launches"; no reference counterpart). */
 uint64_t l1b_kernel_launches(void);

@@ -36,6 +36,8 @@ ABI_SYMBOLS = (
     "l1b_straggler_records",
     "l1b_bound_columns",
     "l1b_fit_pivot_list_seeded",
+    "l1b_last_bound_ms",
+    "l1b_atoms_probe",
 )
 
 L1B_OK = 0
@@ -110,6 +112,10 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_pivot_list_seeded.restype = ctypes.c_int
     lib.l1b_fit_pivot_list_seeded.argtypes = [_vp, _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64, _vp, _vp,
                                               _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_last_bound_ms.restype = ctypes.c_int
+    lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
+    lib.l1b_atoms_probe.restype = ctypes.c_int
+    lib.l1b_atoms_probe.argtypes = [_i64, ctypes.c_int32, ctypes.c_int32, _vp, _vp]
     lib.l1b_set_probe.restype = ctypes.c_int
     lib.l1b_set_probe.argtypes = [_vp]
     _lib = lib

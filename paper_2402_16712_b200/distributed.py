@@ -12,6 +12,11 @@ winner crosses the interconnect:
    strict '<' in ascending pivot order of fit.py:98-102;
 3. the owning rank broadcasts the winning direction (8*m bytes).
 
+With pivot pruning (engine.DeviceFit.shard_winners) one more exchange sits
+between the bound pass and the exact fits: an all-reduce(MIN) of the
+shards' best upper bounds (8 bytes per lambda), so every shard prunes
+against the global best pivot and fits only what can still win overall.
+
 Each pivot is solved on exactly one rank with exactly the single-GPU
 kernels and re-scored with NumPy's summation order, so the result is
 byte-identical for any world size.  There is no data-path collective.
@@ -28,7 +33,7 @@ import torch.distributed as dist
 from .core import FittedLine
 from .engine import DeviceFit, PivotWinner, shard
 
-__all__ = ["shard", "combine_winners", "fit_lines_distributed", "fit_line_distributed",
+__all__ = ["shard", "combine_winners", "ub_exchange", "fit_lines_distributed", "fit_line_distributed",
            "fit_subspace_distributed"]
 
 
@@ -83,9 +88,31 @@ def combine_winners(local: list[PivotWinner | None], m: int, group=None) -> list
     return out
 
 
-def _device_solver(X, lams, p_begin, p_stride, npiv):
+def ub_exchange(group=None) -> Callable[[float], float]:
+    """all-reduce(MIN) of one upper bound per call (the pruning threshold)."""
+    dev = _comm_device(group)
+
+    def exchange(top: float) -> float:
+        t = torch.tensor([top], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        return float(t.item())
+    return exchange
+
+
+def _shard_solve(eng: DeviceFit | None, lams, p_begin, p_stride, npiv, prune: bool, group=None):
+    """One shard's winners; a rank without pivots still joins the exchanges."""
+    ex = ub_exchange(group) if prune else None
+    if npiv == 0:
+        if ex is not None:
+            for _ in lams:
+                ex(float("inf"))
+        return [None] * len(lams)
+    return eng.shard_winners(lams, p_begin, p_stride, npiv, prune=prune, ub_exchange=ex)
+
+
+def _device_solver(X, lams, p_begin, p_stride, npiv, group=None):
     eng = DeviceFit(X, max_pivots=max(1, npiv))
-    return eng.shard_winners(lams, p_begin, p_stride, npiv)
+    return _shard_solve(eng, lams, p_begin, p_stride, npiv, eng.auto_prune(), group)
 
 
 def fit_lines_distributed(X, lams, group=None,
@@ -101,8 +128,10 @@ def fit_lines_distributed(X, lams, group=None,
     m = X.shape[1]
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     p_begin, p_stride, npiv = shard(m, rank, world)
-    solver = solver or _device_solver
-    local = solver(X, lams, p_begin, p_stride, npiv) if npiv > 0 else [None] * len(lams)
+    if solver is None:
+        local = _device_solver(X, lams, p_begin, p_stride, npiv, group)
+    else:
+        local = solver(X, lams, p_begin, p_stride, npiv) if npiv > 0 else [None] * len(lams)
     wins = combine_winners(local, m, group)
     return [FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error, penalty_norm=w.penalty_norm,
                        objective=w.objective) for w in wins]
@@ -138,7 +167,7 @@ def fit_subspace_distributed(data, lam: float, k: int, group=None):
     for t in range(k):
         if eng.absmax() <= 1e-10 * scale:
             return SubspaceFit(tuple(comps), degenerate=True)
-        local = eng.shard_winners([float(lam)], p_begin, p_stride, npiv) if npiv > 0 else [None]
+        local = _shard_solve(eng, [float(lam)], p_begin, p_stride, npiv, eng.auto_prune(), group)
         w = combine_winners(local, m, group)[0]
         comps.append(FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,
                                 penalty_norm=w.penalty_norm, objective=w.objective))

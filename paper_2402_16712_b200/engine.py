@@ -269,22 +269,27 @@ class DeviceFit:
         return self._scale
 
     def shard_winners(self, lams, p_begin: int = 0, p_stride: int = 1,
-                      npiv: int | None = None, prune: bool | None = None) -> list[PivotWinner]:
+                      npiv: int | None = None, prune: bool | None = None,
+                      ub_exchange=None) -> list[PivotWinner | None]:
         """Exact winner of the shard for every lambda (fit.py:98-102 semantics).
 
-        With ``prune`` (None: when the fit is large enough to pay for it)
-        every pivot is first bounded by one FP32 pass
+        With ``prune`` (None: auto_prune()) every pivot is first bounded by one FP32 pass
         (l1b_bound_pivots) and only the pivots whose lower bound does not
         exceed the smallest upper bound are fitted exactly -- the others
         provably cannot win, so the result is the same as fitting all.
+
+        ``ub_exchange(top) -> global top`` (sharded fits) replaces the
+        shard's best upper bound by the best over all shards before pruning;
+        a shard whose pivots are all provably beaten then returns None for
+        that lambda.  Every rank must call it once per lambda when pruning.
         """
         lam = np.atleast_1d(np.asarray(lams, dtype=np.float64))
         if npiv is None:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         all_piv = p_begin + p_stride * np.arange(npiv, dtype=np.int64)
         out = []
-        if prune is None:  # auto: bounding costs a pass of its own, not worth it for small fits
-            prune = npiv > 32 and npiv * self.m * self.n >= (1 << 24)
+        if prune is None:
+            prune = self.auto_prune()
         if not prune:
             V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
             obj_h = obj.cpu().numpy()
@@ -292,7 +297,13 @@ class DeviceFit:
         for l in range(lam.size):
             lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
             top = float(np.min(ub))
+            if ub_exchange is not None:
+                top = float(ub_exchange(top))  # the best upper bound over every shard
             keep = np.nonzero(~(lb > self._prune_threshold(top)))[0]  # NaN-safe: keep unless provably worse
+            if keep.size == 0:  # another shard holds a pivot provably better than all of ours
+                self.last_candidates = 0
+                out.append(None)
+                continue
             seed, seed_n = keep, npiv  # positions in the last bound call's pivot list
             if keep.size > REFINE_MIN:
                 # second stage on the survivors: every further pass
@@ -308,6 +319,12 @@ class DeviceFit:
             V, err, pen, obj = self.fit_pivot_list_seeded(float(lam[l]), piv, seed, seed_n)
             out.append(self._winner(float(lam[l]), piv, V[0], obj.cpu().numpy()[0]))
         return out
+
+    def auto_prune(self) -> bool:
+        """Whether shard_winners bounds before fitting: the bound pass costs a
+        pass of its own, not worth it for small fits.  Depends on the matrix
+        only, so every rank of a sharded fit decides alike."""
+        return self.m > 32 and self.m * self.m * self.n >= (1 << 24)
 
     def _prune_threshold(self, top: float) -> float:
         if not np.isfinite(top):

@@ -74,3 +74,43 @@ def test_sharded_fit_matches_single_process(world):
             piv, vb, z, e, pn, lam = res[r][k]
             assert piv == w.preserved and vb == w.v.tobytes()
             assert z == w.objective and e == w.error and pn == w.penalty_norm and lam == lams[k]
+
+
+def _exchange_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2402_16712_b200.distributed import _shard_solve, ub_exchange
+        ex = ub_exchange()
+        tops = [5.0 + rank, float("inf") if rank == 1 else 2.0 - rank, 1e300 * (rank + 1)]
+        got = [ex(t) for t in tops]
+        # a rank that owns no pivots still joins one exchange per lambda
+        if rank == world - 1:
+            none = _shard_solve(None, [0.0, 1.0], 0, 1, 0, True)
+            assert none == [None, None]
+        else:
+            got += [ex(float(rank)), ex(-float(rank))]
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ub_exchange_is_global_min(world):
+    """The pruning threshold exchange (all-reduce MIN), including ranks without pivots."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [5.0, min(2.0 - r for r in range(world) if r != 1), 1e300]
+    for r in range(world):
+        assert res[r][:3] == want
+        if r != world - 1:
+            assert res[r][3:] == [0.0, -float(world - 2)]

@@ -19,7 +19,7 @@ import torch
 import oracle
 import paper_2402_16712_b200 as l1b
 from conftest import TOY, iter_random_small, iter_random_small_lines, load_golden
-from paper_2402_16712_b200.engine import DeviceFit
+from paper_2402_16712_b200.engine import DeviceFit, shard
 
 pytestmark = pytest.mark.gpu
 
@@ -419,3 +419,23 @@ def test_seeded_exact_fit_equals_batched_fit(m, n):
                 # in NumPy order either way)
                 np.testing.assert_allclose(e1.cpu().numpy(), e0, rtol=1e-12)
                 np.testing.assert_allclose(o1.cpu().numpy(), o0, rtol=1e-12)
+
+
+def test_sharded_pruning_with_global_threshold():
+    """Two interleaved pivot shards pruned against the global best upper bound
+    (what distributed.ub_exchange provides) combine to the unsharded winner;
+    a shard may keep no pivot at all."""
+    d, _ = l1b.gen_line_data(120, 1500, seed=8, noise_scale=1.0)
+    X = d.values
+    T = float(np.abs(X).sum(axis=0).max())
+    m = X.shape[1]
+    eng = DeviceFit(X)
+    for lam in (1.0, 0.2 * T):
+        want = eng.shard_winners([lam], prune=False)[0]
+        shards = [shard(m, r, 3) for r in range(3)]
+        tops = [float(np.min(eng.bound_pivots(lam, *sh)[1])) for sh in shards]
+        wins = [eng.shard_winners([lam], *sh, prune=True, ub_exchange=lambda t: min(tops))[0] for sh in shards]
+        wins = [w for w in wins if w is not None]
+        best = min(wins, key=lambda w: (w.objective, w.pivot))
+        assert best.pivot == want.pivot and best.v.tobytes() == want.v.tobytes()
+        assert best.objective == want.objective

@@ -23,7 +23,7 @@ shapes = {"c2": (2000, 2000), "c4": (500, 100000), "c5": (10000, 10000)}
 m, n = shapes[a.config]
 d, _ = l1b.gen_line_data(m, n, seed=0, noise_scale=1.0)
 eng = DeviceFit(np.array(d.values))
-eng.prepare()
+# DeviceFit() already ran K0 (prepare)
 w = eng.shard_winners([a.lam])[0]
 torch.cuda.synchronize()
 print("winner", w.pivot, repr(w.objective), "exactly fitted pivots", eng.last_candidates)
