@@ -32,12 +32,22 @@ constexpr int kBPairs = 4;                 // pivot pairs per k_bound CTA (8 piv
 constexpr int kBWarps = 2 * kBPairs;       // two row halves per pair
 constexpr int kBThreads = kBWarps * 32;
 constexpr int kBSlots = kBPairs * 32;      // histogram columns: (pair, target)
-constexpr int kBRows = 64;                 // rows per staged chunk
+#ifndef KB_ROWS
+#define KB_ROWS 64
+#endif
+#ifndef KB_STAGES
+#define KB_STAGES 3
+#endif
+#ifndef KB_UNROLL
+#define KB_UNROLL 2
+#endif
+constexpr int kBRows = KB_ROWS;            // rows per staged chunk
 constexpr int kBTile = kBRows * 32 * 4;    // x_ij float tile [row][32 targets]
 constexpr int kBPlane = kBRows * kWarps * 8;   // (y32, x_ip32) [row][8 pivots]
 constexpr int kBPlaneU = kBRows * kWarps * 4;  // 32-bit weights [row][8 pivots]
 constexpr int kBStage = kBTile + kBPlane + kBPlaneU;
-constexpr int kBStages = 3;
+constexpr int kBStages = KB_STAGES;
+constexpr int kBUnroll = KB_UNROLL;        // 8-row groups per main-loop iteration
 constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [problem][bin][slot], exact 32-bit sums
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 // bracket half-width in sample ranks: narrow for the one-pass bound (tight
@@ -62,53 +72,90 @@ __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double 
   // (a chunk sums 16 pairwise 4-row sums: relative error <= 18 u)
   const double eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
   const double fc = ec + lam * fabs(c);
-  // edges e_k = lo + k w (k = 0..62); C_k = weight with r < e_k = slots 0..k
+  // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
+  // (slots 0..k).  The subgradient bounds at edge k are
+  //   glo(k) = 2 (C_k - dC) - T + lam sp(k) <= g(e_k+),  sp(k) = e_k >= 0 ? 1 : -1,
+  //   ghi(k) = 2 (C_k + dC) - T + lam sm(k) >= g(e_k-),  sm(k) = e_k >  0 ? 1 : -1,
+  // on bin [e_k, e_k+1] g lies in [glo(k), ghi(k+1)], and their integrals
+  //   Ilo(k) = sum_{q<k} w glo(q),  Ihi(k) = sum_{q<k} w ghi(q+1)
+  // need only the exact integer prefix sums Cu_k, SC_k = sum_{q<k} Cu_q and
+  // the edge-sign counts, so the walk over the edges is integer-only.
   auto edge = [&](int k) { return lo + (double)k * w; };
-  // one walk over the edges: C_k = weight with r < e_k (slots 0..k); the
-  // subgradient bounds Glo(k) <= g(e_k+), Ghi(k) >= g(e_k-) are monotone in k,
-  // so kL (last edge with Ghi <= 0) and kR (first with Glo >= 0) are seen in
-  // order; I(k) = sum_{q<k} w g(q) integrates the per-bin bounds from e_0
+  int z0 = min(kNB - 1, max(0, (int)ceil(-lo / w)));  // edges e_0 .. e_z0-1 are < 0
+  while (z0 > 0 && edge(z0 - 1) >= 0.0) --z0;
+  while (z0 < kNB - 1 && edge(z0) < 0.0) ++z0;
+  int z1 = z0;  // edges e_0 .. e_z1-1 are <= 0
+  while (z1 < kNB - 1 && edge(z1) <= 0.0) ++z1;
   const int kc = min(kNI - 1, max(0, (int)floor((c - lo) / w)));
+  // integer thresholds, rounded so that passing them implies the double test:
+  // ghi(k) <= 0 <=> Cu_k <= (T - 2 dC - lam sm) / 2q;  glo(k) >= 0 <=> Cu_k >= (T + 2 dC - lam sp) / 2q
+  const double iq2 = 0.5 / q;
+  auto thr_le = [&](double x) -> long long {
+    x = x * iq2 * (1.0 - 0x1p-44) - 0x1p-8;
+    return x < 0.0 ? -1LL : (x >= 0x1p62 ? (1LL << 62) : (long long)floor(x));
+  };
+  auto thr_ge = [&](double x) -> long long {
+    x = x * iq2 * (1.0 + 0x1p-44) + 0x1p-8;
+    return x <= 0.0 ? 0LL : (x >= 0x1p62 ? (1LL << 62) : (long long)ceil(x));
+  };
+  const long long tLm = thr_le(T - 2.0 * dC + lam), tLp = thr_le(T - 2.0 * dC - lam);  // sm = -1 / +1
+  const long long tRm = thr_ge(T + 2.0 * dC + lam), tRp = thr_ge(T + 2.0 * dC - lam);  // sp = -1 / +1
   int kL = -1, kR = kNB - 1;
-  double CL = 0.0, CR = T;
-  double Ilo = 0.0, Ihi = 0.0, IloC = 0.0, IhiC = 0.0, IloL = 0.0, IhiL = 0.0, IloR = 0.0, IhiR = 0.0;
-  double gloC = 0.0, ghiC = 0.0, gloL = 0.0;
+  long long CuL = 0, SCL = 0, CuR = 0, SCR = 0, CuC = 0, SCC = 0, CuC1 = 0, Cu0 = 0, Cu62 = 0, SC62 = 0;
   {
-    double C = (double)h[0] * q;
-    double ghiE = 2.0 * (C + dC) - T + (edge(0) > 0.0 ? lam : -lam);
-    double gloE = 2.0 * (C - dC) - T + (edge(0) >= 0.0 ? lam : -lam);
+    // Cu_k < 2^31 (the weights sum to Tq / 2^21 + n / 2): 32-bit compares
+    const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
+    const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
+    const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
+    const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
+    unsigned Cu = 0;
+    long long SC = 0;
+    Cu0 = h[0];
     for (int k = 0; k <= kNI; ++k) {
-      // at edge k: ghiE / gloE are its bounds, C its cumulative weight
-      if (ghiE <= 0.0) { kL = k; CL = C; IloL = Ilo; IhiL = Ihi; gloL = gloE; }
-      if (kR == kNB - 1 && gloE >= 0.0) { kR = k; CR = C; IloR = Ilo; IhiR = Ihi; }
-      if (k == kc) { IloC = Ilo; IhiC = Ihi; }
-      if (k == kNI || (kR < kNB - 1 && k > kc)) break;  // everything needed is captured
-      const double Cn = C + (double)h[(k + 1) * hs] * q;
-      const double ghiN = 2.0 * (Cn + dC) - T + (edge(k + 1) > 0.0 ? lam : -lam);
-      const double gloN = 2.0 * (Cn - dC) - T + (edge(k + 1) >= 0.0 ? lam : -lam);
-      // g on [e_k, e_k+1] lies in [gloE, ghiN]
-      if (k == kc) { gloC = gloE; ghiC = ghiN; }
-      Ilo += w * gloE;
-      Ihi += w * ghiN;
-      C = Cn;
-      ghiE = ghiN;
-      gloE = gloN;
+      Cu += h[k * hs];  // Cu_k; SC = SC_k
+      const bool pl = k >= z1, pr = k >= z0;
+      if (pl ? (hasL_p & (Cu <= uLp)) : (hasL_m & (Cu <= uLm))) { kL = k; CuL = Cu; SCL = SC; }
+      const bool r = pr ? (hasR_p & (Cu >= uRp)) : (hasR_m & (Cu >= uRm));
+      if (r & (kR == kNB - 1)) { kR = k; CuR = Cu; SCR = SC; }
+      if (k == kc) { CuC = Cu; SCC = SC; }
+      if (k == kc + 1) CuC1 = Cu;
+      Cu62 = Cu;
+      SC62 = SC;
+      if ((kR < kNB - 1) & (k > kc)) break;  // everything needed is captured
+      SC += Cu;
     }
   }
+  const double q2 = 2.0 * q;
+  auto glo = [&](int k, long long Cu) { return q2 * (double)Cu - 2.0 * dC - T + (k >= z0 ? lam : -lam); };
+  auto ghi = [&](int k, long long Cu) { return q2 * (double)Cu + 2.0 * dC - T + (k >= z1 ? lam : -lam); };
+  auto Ilo = [&](int k, long long SC) {  // SP(k) = sum_{q<k} sp(q) = k - 2 min(k, z0)
+    return w * (q2 * (double)SC - (double)k * (2.0 * dC + T) + lam * (double)(k - 2 * min(k, z0)));
+  };
+  auto Ihi = [&](int k, long long SC, long long Cu) {  // SM1(k) = sum_{q=1..k} sm(q)
+    const int le = max(0, min(k, z1 - 1));
+    return w * (q2 * (double)(SC + Cu - Cu0) + (double)k * (2.0 * dC - T) + lam * (double)(k - 2 * le));
+  };
+  const double IloC = Ilo(kc, SCC), IhiC = Ihi(kc, SCC, CuC);
+  const double gloC = glo(kc, CuC), ghiC = ghi(kc + 1, CuC1), gloL = kL >= 0 ? glo(kL, CuL) : 0.0;
+  const double CL = q * (double)CuL, CR = kR <= kNI ? q * (double)CuR : T;
   // f at e_kc from f(c), then at any edge k from e_kc
   const double dc = c - edge(kc);
   const double fkc_lo = fc - dc * ghiC, fkc_hi = fc - dc * gloC;
-  auto f_lo = [&](int k, double Ilk, double Ihk) { return k >= kc ? fkc_lo + (Ilk - IloC) : fkc_lo - (IhiC - Ihk); };
-  auto f_hi = [&](int k, double Ilk, double Ihk) { return k >= kc ? fkc_hi + (Ihk - IhiC) : fkc_hi - (IloC - Ilk); };
+  auto f_lo = [&](int k, long long SC, long long Cu) {
+    return k >= kc ? fkc_lo + (Ilo(k, SC) - IloC) : fkc_lo - (IhiC - Ihi(k, SC, Cu));
+  };
+  auto f_hi = [&](int k, long long SC, long long Cu) {
+    return k >= kc ? fkc_hi + (Ihi(k, SC, Cu) - IhiC) : fkc_hi - (IloC - Ilo(k, SC));
+  };
   const double f0 = colsum;  // f(0): the dead value, exact
   double lb, ub = fmin(fc + eps, f0);
   const double eL = kL >= 0 ? edge(kL) : -INFINITY, eR = kR <= kNI ? edge(kR) : INFINITY;
   if (kL >= 0 && kR <= kNI && kL <= kR) {
-    lb = f_lo(kL, IloL, IhiL) - eps + fmin(0.0, gloL) * (eR - eL);
-    ub = fmin(ub, fmin(f_hi(kL, IloL, IhiL), f_hi(kR, IloR, IhiR)) + eps);
+    lb = f_lo(kL, SCL, CuL) - eps + fmin(0.0, gloL) * (eR - eL);
+    ub = fmin(ub, fmin(f_hi(kL, SCL, CuL), f_hi(kR, SCR, CuR)) + eps);
   } else {
     lb = 0.0;  // the optimum lies beyond the bracket: only the trivial bound
-    if (kL == kNI) ub = fmin(ub, f_hi(kNI, Ilo, Ihi) + eps);
+    if (kL == kNI) ub = fmin(ub, f_hi(kNI, SC62, Cu62) + eps);
   }
   if (eL <= 0.0 && 0.0 <= eR) {
     // the penalty's kink: g(0-) <= 2 W(r < eR) - T - lam, g(0+) >= 2 W(r < eL) - T + lam;
@@ -130,21 +177,39 @@ __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double 
   }
 }
 
-// Sample bracket of one problem: float ratios of 32 strided rows, bitonic
-// sorted in registers; returns the bracket +-kDelta ranks around the
-// estimated crossing and that estimate (the residual's reference point).
+// Sample bracket of one problem: float ratios of 32 strided rows, sorted in
+// registers as packed 32-bit keys (order-preserving image of the ratio, low 8
+// bits replaced by the row's weight quantised to 1/255 of the sample's
+// largest), so every compare-exchange is a min and a max; returns the
+// bracket +-delta ranks around the estimated crossing, that estimate (the
+// residual's reference point) and the sample's extremes.  The bracket only
+// steers the histogram: any bracket gives rigorous bounds.
+__device__ __forceinline__ unsigned f2key(float f) {
+  const unsigned b = __float_as_uint(f);
+  return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned k) {
+  return __uint_as_float(k ^ (((unsigned)((int)~k >> 31)) | 0x80000000u));
+}
+
 __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
                                                double unit, int delta, float* lo, float* hi, float* cen,
                                                float* smin, float* smax) {
   const int64_t n = P.n;
   float sr[kSample], sw[kSample];
+  float wmax = 0.f;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
     const int64_t r = ((2 * s + 1) * n) / (2 * kSample);
     const float2 f = P.pf[p * P.np + r];
     sr[s] = P.Xft[tbase + r * 32 + lane] * f.x;
     sw[s] = fabsf(f.y);
+    wmax = fmaxf(wmax, sw[s]);
   }
+  const float wsc = wmax > 0.f ? 255.f / wmax : 0.f;
+  unsigned key[kSample];
+#pragma unroll
+  for (int s = 0; s < kSample; ++s) key[s] = (f2key(sr[s]) & 0xffffff00u) | (unsigned)__float2uint_rn(sw[s] * wsc);
 #pragma unroll
   for (int k = 2; k <= kSample; k <<= 1) {
 #pragma unroll
@@ -153,43 +218,42 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
       for (int i = 0; i < kSample; ++i) {
         const int l = i ^ jj;
         if (l > i) {
+          const unsigned a = key[i], b = key[l];
           const bool up = (i & k) == 0;
-          const bool x = up ? (sr[i] > sr[l]) : (sr[i] < sr[l]);
-          const float ta = sr[i], tb = sr[l], wa = sw[i], wb = sw[l];
-          sr[i] = x ? tb : ta;
-          sr[l] = x ? ta : tb;
-          sw[i] = x ? wb : wa;
-          sw[l] = x ? wa : wb;
+          key[i] = up ? min(a, b) : max(a, b);
+          key[l] = up ? max(a, b) : min(a, b);
         }
       }
     }
   }
-  float ws = 0.f, wn = 0.f;
+  unsigned ws = 0, wn = 0;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
-    ws += sw[s];
-    wn += sr[s] < 0.f ? sw[s] : 0.f;
+    const unsigned wq = key[s] & 0xffu;
+    ws += wq;
+    wn += key[s] < 0x80000000u ? wq : 0u;  // ratio < 0
   }
   const float rho = Tq > 0.0 ? (float)(P.lam / (Tq * unit)) : 0.f;
-  const float d = ws > 0.f ? 1.f - 2.f * wn / ws : 1.f;
+  const float d = ws > 0 ? 1.f - 2.f * (float)wn / (float)ws : 1.f;
   const float f = d < -rho ? 0.5f * (1.f + rho) : (d >= rho ? 0.5f * (1.f - rho) : 0.5f);
-  const float t = f * ws;
-  float c = 0.f;
+  const float t = f * (float)ws;
+  unsigned c = 0;
   int sstar = kSample - 1;
-  bool got = false;
+  bool got = false;  // first s with prefix weight > t
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
-    c += sw[s];
-    if (!got && c > t) { sstar = s; got = true; }
+    c += key[s] & 0xffu;
+    if (!got && (float)c > t) { sstar = s; got = true; }
   }
   const int lo_i = max(sstar - delta, 0), hi_i = min(sstar + delta, kSample - 1);
-  float l = 0.f, hh = 0.f, ce = 0.f;
+  unsigned kl = 0, kh = 0, kce = 0;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
-    if (s == lo_i) l = sr[s];
-    if (s == hi_i) hh = sr[s];
-    if (s == sstar) ce = sr[s];
+    if (s == lo_i) kl = key[s];
+    if (s == hi_i) kh = key[s];
+    if (s == sstar) kce = key[s];
   }
+  float l = key2f(kl & 0xffffff00u), hh = key2f((kh & 0xffffff00u) | 0xffu), ce = key2f(kce & 0xffffff00u);
   if (!(hh > l)) {  // degenerate sample: a tiny bracket around it
     const float e = fmaxf(fabsf(l), 1e-30f) * 1e-3f;
     l -= e;
@@ -198,8 +262,8 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
   *lo = l;
   *hi = hh;
   *cen = fminf(fmaxf(ce, l), hh);
-  *smin = sr[0];
-  *smax = sr[kSample - 1];
+  *smin = key2f(key[0] & 0xffffff00u);
+  *smax = key2f((key[kSample - 1] & 0xffffff00u) | 0xffu);
 }
 
 // NPASS = 1: one pass over the sample bracket.  NPASS > 1 (refinement for
@@ -216,7 +280,8 @@ template <int NPASS>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
-  __shared__ __align__(8) unsigned long long full[kBStages], empty[kBStages];
+  __shared__ __align__(8) unsigned long long full[kBStages];
+  __shared__ unsigned done[kBStages];   // warps finished with the stage's chunk
   __shared__ float sbr[2][5][kBSlots];  // brackets: problem t's (lo, hi, cen, smin, smax) per slot
   __shared__ double sec[kBSlots];       // e_j(c) of problem 0 from the other half
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -243,7 +308,11 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   {  // each half samples one problem's bracket; both halves need both
     const bool h = half != 0;
     float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
+#ifndef KB_NOSAMPLE
     if (h ? act[1] : act[0])
+#else
+    if (false)
+#endif
       sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0],
                      NPASS == 1 ? kBDelta1 : kBDeltaN, &b0, &b1, &b2, &b3, &b4);
     float* d = &sbr[half][0][slot];
@@ -253,12 +322,26 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     d[3 * kBSlots] = b3;
     d[4 * kBSlots] = b4;
   }
+  const int64_t nch = (n + kBRows - 1) / kBRows;
+  const int64_t nseq = NPASS * nch;  // chunks consumed over all passes, in order
+  // stage refill: the chunk with sequence number g goes to stage g % kBStages
+  auto issue = [&](int64_t g) {
+    const int st = (int)(g % kBStages);
+    const int64_t i0 = (g % nch) * kBRows;
+    unsigned char* base = smem + (size_t)st * kBStage;
+    fence_proxy_async();
+    mbar_expect_tx(&full[st], (unsigned)kBStage);
+    bulk_g2s(base, P.Xft + tbase + i0 * 32, kBTile, &full[st]);
+    bulk_g2s(base + kBTile, P.gpf + gbase + i0 * 8, kBPlane, &full[st]);
+    bulk_g2s(base + kBTile + kBPlane, P.gwu + gbase + i0 * 8, kBPlaneU, &full[st]);
+  };
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBWarps);
+      done[s] = 0u;
     }
     mbar_fence_init();
+    for (int64_t g = 0; g < min((int64_t)kBStages, nseq); ++g) issue(g);
   }
   __syncthreads();
 #pragma unroll
@@ -270,28 +353,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     smax[t] = sbr[t][4][slot];
   }
 
-  const int64_t nch = (n + kBRows - 1) / kBRows;
-  unsigned ephase = 0, fphase = 0;
-  int64_t issued = 0;  // chunks issued over all passes (stage = issued % kBStages)
-  auto issue = [&](int64_t c) {
-    if (warp != 0) return;
-    const int st = (int)(issued % kBStages);
-    if (issued >= kBStages) {
-      mbar_wait(&empty[st], (ephase >> st) & 1u);
-      ephase ^= 1u << st;
-    }
-    ++issued;
-    if (lane == 0) {
-      const int64_t i0 = c * kBRows;
-      unsigned char* base = smem + (size_t)st * kBStage;
-      fence_proxy_async();
-      mbar_expect_tx(&full[st], (unsigned)kBStage);
-      bulk_g2s(base, P.Xft + tbase + i0 * 32, kBTile, &full[st]);
-      bulk_g2s(base + kBTile, P.gpf + gbase + i0 * 8, kBPlane, &full[st]);
-      bulk_g2s(base + kBTile + kBPlane, P.gwu + gbase + i0 * 8, kBPlaneU, &full[st]);
-    }
-    __syncwarp();
-  };
+  unsigned fphase = 0;
   const bool busy = __any_sync(0xffffffffu, act[0] || act[1]);
   int64_t consumed = 0;  // chunks consumed over all passes
   double ec0 = 0.0, ec1 = 0.0;  // this half's share of e_j(c) of both problems (last pass)
@@ -313,19 +375,21 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     }
     __syncthreads();
     const int64_t c0 = consumed;
-    for (int64_t c = 0; c < min((int64_t)(kBStages - 1), nch); ++c) issue(c);
     for (int64_t c = 0; c < nch; ++c) {
-      if (c + kBStages - 1 < nch) issue(c + kBStages - 1);
       const int st = (int)((c0 + c) % kBStages);
       mbar_wait(&full[st], (fphase >> st) & 1u);
       fphase ^= 1u << st;
+#ifndef KB_NOCOMPUTE
       if (busy) {
+#else
+      if (false) {
+#endif
         const unsigned char* sb = smem + (size_t)st * kBStage;
         const float* ta = (const float*)sb;
         const float4* pf4 = (const float4*)(sb + kBTile) + pair;  // (y, x_ip) of pivots 2w', 2w'+1
         const uint2* pu2 = (const uint2*)(sb + kBTile + kBPlane) + pair;  // their 32-bit weights
         float r0acc = 0.f, r1acc = 0.f;
-#pragma unroll 2
+#pragma unroll kBUnroll
         for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
           float av[4];
           float4 yw[4];
@@ -345,6 +409,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
             a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
                                 (unsigned)(kBSlots * 4);
           }
+#ifndef KB_NORESID
           if (resid) {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
             float e0[4], e1[4];
 #pragma unroll
@@ -355,11 +420,17 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
             r0acc += (e0[0] + e0[1]) + (e0[2] + e0[3]);
             r1acc += (e1[0] + e1[1]) + (e1[2] + e1[3]);
           }
+#endif
           // fire-and-forget shared adds (the other half adds into the same bins)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
+#ifndef KB_NOATOM
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[u]), "r"(wu[u].x));
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[u]), "r"(wu[u].y));
+#else
+            r0acc += __uint_as_float(a0[u] ^ wu[u].x);
+            r1acc += __uint_as_float(a1[u] ^ wu[u].y);
+#endif
           }
         }
         if (resid) {
@@ -368,7 +439,19 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) {
+        // the last warp done with the stage refills it (no producer waits)
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&done[st]))
+                     : "memory");
+        if (old == kBWarps - 1) {
+          done[st] = 0u;
+          const int64_t g = c0 + c + kBStages;
+          if (g < nseq) issue(g);
+        }
+      }
     }
     consumed += nch;
     __syncthreads();  // both halves' adds are in
@@ -435,10 +518,12 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     return;
   }
   const double ut = h ? unit[1] : unit[0];
-  double lb, ub;
+  double lb = 0.0, ub = 0.0;
+#ifndef KB_NOEPI
   column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
                 (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam,
                 P.colsum[j], n, &lb, &ub, &P.BRK[o]);
+#endif
   P.LB[o] = lb;
   P.UB[o] = ub;
 }
