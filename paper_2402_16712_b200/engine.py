@@ -69,6 +69,35 @@ def shard(m: int, rank: int, world: int) -> tuple[int, int, int]:
     return rank, world, npiv
 
 
+_STAGING: dict = {}
+_STAGE_DOUBLES = 1 << 21  # 16 MB pinned chunks
+
+
+def _upload(Xh: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Host numpy -> device through two reused pinned chunks: the CPU copy of
+    chunk i+1 into pinned memory overlaps the DMA of chunk i (instead of
+    pinning the whole matrix, then copying it)."""
+    key = (device.type, device.index)
+    if key not in _STAGING:
+        with torch.cuda.device(device):
+            _STAGING[key] = [(torch.empty(_STAGE_DOUBLES, dtype=torch.float64).pin_memory(), torch.cuda.Event())
+                             for _ in range(2)]
+    stage = _STAGING[key]
+    src = torch.from_numpy(Xh.reshape(-1))
+    with torch.cuda.device(device):
+        dst = torch.empty(Xh.shape, dtype=torch.float64, device=device)
+        flat = dst.view(-1)
+        stream = torch.cuda.current_stream(device)
+        for i, off in enumerate(range(0, src.numel(), _STAGE_DOUBLES)):
+            k = min(_STAGE_DOUBLES, src.numel() - off)
+            buf, ev = stage[i & 1]
+            ev.synchronize()  # the DMA that last read this chunk has finished
+            buf[:k].copy_(src[off:off + k])
+            flat[off:off + k].copy_(buf[:k], non_blocking=True)
+            ev.record(stream)
+    return dst
+
+
 class DeviceFit:
     """A data matrix resident on one GPU plus everything a fit needs."""
 
@@ -83,8 +112,7 @@ class DeviceFit:
             Xd = X.to(device=self.device, dtype=torch.float64).contiguous()
         else:
             Xh = np.ascontiguousarray(X, dtype=np.float64)
-            Xd = torch.from_numpy(Xh).pin_memory().to(self.device, non_blocking=True) \
-                if Xh.size >= (1 << 16) else torch.from_numpy(Xh).to(self.device)
+            Xd = _upload(Xh, self.device) if Xh.size >= (1 << 16) else torch.from_numpy(Xh).to(self.device)
         if Xd.dim() != 2:
             raise ValueError(f"expected a 2-d array, got shape {tuple(Xd.shape)}")
         self.X = Xd
