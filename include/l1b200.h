@@ -85,11 +85,10 @@ int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_
                      int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
 /* l1b_bound_pivots for a pivot list (host memory) with 1 to 3 passes per
- * problem: every further pass re-histograms the bin of the subgradient's
- * sign change (62 sub-bins; or extends the bracket when the optimum lay
- * outside it) and the last sums the residual at its centre, which tightens
- * the bounds by orders of magnitude per pass -- used on the pivots the
- * one-pass bounds could not rule out. */
+ * problem: every further pass re-histograms the range where the previous
+ * one proved the optimum lies (62 sub-bins; or extends the range when the
+ * optimum lay outside it), which tightens the bounds by orders of magnitude
+ * per pass -- used on the pivots the one-pass bounds could not rule out. */
 int l1b_bound_pivot_list(const double* d_X, int64_t n, int64_t m, double lam, const int64_t* h_pivots,
                          int64_t npiv, int32_t passes, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes,
                          void* stream);
@@ -140,6 +139,15 @@ int l1b_set_probe(uint64_t* d_buf);
  * Synchronises the stream. */
 int l1b_straggler_records(int64_t n, int64_t m, int64_t npiv, const void* d_ws, size_t ws_bytes, void* h_out,
                           int64_t max_records, void* stream);
+
+/* One more bounding pass for a pivot list that the previous l1b_bound_*
+ * call on this workspace covered: pivot k was entry h_from[k] of that call's
+ * list of from_npiv pivots, and its pass starts from the range that call
+ * left for each (pivot, target) problem.  A cascade (all pivots, then the
+ * survivors, then theirs) costs one pass per level per surviving pivot. */
+int l1b_bound_pivot_list_continue(const double* d_X, int64_t n, int64_t m, double lam, const int64_t* h_pivots,
+                                  int64_t npiv, const int64_t* h_from, int64_t from_npiv, double* d_lb,
+                                  double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Exact fit (as l1b_fit_pivot_list, one lambda) of a short pivot list that
  * a preceding l1b_bound_pivot_list call on this workspace bounded: pivot k

@@ -36,6 +36,7 @@ ABI_SYMBOLS = (
     "l1b_straggler_records",
     "l1b_bound_columns",
     "l1b_fit_pivot_list_seeded",
+    "l1b_bound_pivot_list_continue",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -112,6 +113,9 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_pivot_list_seeded.restype = ctypes.c_int
     lib.l1b_fit_pivot_list_seeded.argtypes = [_vp, _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64, _vp, _vp,
                                               _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_pivot_list_continue.restype = ctypes.c_int
+    lib.l1b_bound_pivot_list_continue.argtypes = [_vp, _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64, _vp,
+                                                  _vp, _vp, _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

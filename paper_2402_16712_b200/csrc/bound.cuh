@@ -59,7 +59,8 @@ constexpr int kBDelta1 = 7, kBDeltaN = 10;
 // e_j(c) = ec, the exact pivot weight T and the column's sum_i |x_ij| (f(0)).
 __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double q, double lo, double hi, double c,
                                               double ec, double T, double lam, double colsum, int64_t n,
-                                              double* lbo, double* ubo, double2* range) {
+                                              float smin, float smax, double* lbo, double* ubo, double2* range,
+                                              float2* next) {
   const double w = (hi - lo) / (double)kNI;
   // margins: the 32-bit weights are within q/2 of |x_ip| each (so any
   // cumulative weight within n q / 2), the residual terms within 2^-22 of
@@ -175,6 +176,28 @@ __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double 
   } else {
     *range = make_double2(-INFINITY, INFINITY);
   }
+  // the next pass's range: between the edges where the optimum provably lies
+  // (a little wider), or, when a side is not in the bracket, extended there
+  const float flo = (float)lo, fhi = (float)hi, span = fhi - flo;
+  float a, b;
+  if (kL >= 0 && kR <= kNI) {
+    a = (float)edge(max(0, min(kL, kR - 1)));
+    b = (float)edge(min(kNI, max(kR, kL + 1)));
+  } else if (kR <= kNI) {  // optimum at or below lo
+    a = fminf(smin, flo) - 2.f * span;
+    b = (float)edge(kR);
+  } else if (kL >= 0) {  // at or above the last edge
+    a = (float)edge(kL);
+    b = fmaxf(smax, fhi) + 2.f * span;
+  } else {  // no edge is decisive (margins dominate): keep the range
+    a = flo;
+    b = fhi;
+  }
+  const float mg = 0.05f * (b - a);
+  a -= mg;
+  b += mg;
+  if (!(b > a)) b = a + fmaxf(fabsf(a), 1e-30f) * 1e-6f;
+  *next = make_float2(a, b);
 }
 
 // Sample bracket of one problem: float ratios of 32 strided rows, sorted in
@@ -266,17 +289,21 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
   *smax = key2f((key[kSample - 1] & 0xffffff00u) | 0xffu);
 }
 
-// NPASS = 1: one pass over the sample bracket.  NPASS > 1 (refinement for
-// the pivots the first stage could not rule out): every pass but the last
-// only histograms its range; the next re-histograms the range where the
-// optimum provably lies with 62 sub-bins, so the integration error shrinks
-// with the square of the bin width; the last pass also sums e_j at its centre.
+// One bounding pass per (pivot, target) problem.  CONT = false: the range
+// comes from a row sample (sample_bracket, half-width P.delta ranks).
+// CONT = true (refinement for the pivots an earlier pass could not rule out):
+// the range is the one the previous pass over the same problem left in
+// P.NEXTr (row P.seeds[k] of that pass's pivot list, or k), i.e. where that
+// pass proved the optimum lies, so the 62 bins shrink by ~60x per pass and
+// the integration error with their square.  Every pass also writes the next
+// range (P.NEXTw), the seed range for the exact solver (P.BRK) and the
+// per-column bounds (P.LB / P.UB).
 //
 // Threads: warps w and w + 4 own the same pivot pair (2w', 2w'+1, w' = w % 4)
 // and target (lane) and split each chunk's rows (alternate 4-row groups);
 // both add into the problem's one histogram with shared-memory atomics, so
 // the CTA holds 8 warps for the histogram space of 4.
-template <int NPASS>
+template <bool CONT>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
@@ -294,7 +321,6 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   int64_t kk[2], p[2];
   bool ok[2], degen[2], act[2];
   double Tq[2], unit[2];
-  float lo[2], hi[2], cen[2], smin[2], smax[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     kk[t] = (int64_t)blockIdx.y * kWarps + 2 * pair + t;
@@ -305,16 +331,21 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     Tq[t] = ok[t] && !degen[t] ? P.tq[p[t]] : 0.0;
     unit[t] = ldexp(1.0, ok[t] && !degen[t] ? -P.spow[p[t]] : 0);
   }
-  {  // each half samples one problem's bracket; both halves need both
+  {  // each half prepares one problem's bracket; both halves need both
     const bool h = half != 0;
     float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
-#ifndef KB_NOSAMPLE
-    if (h ? act[1] : act[0])
-#else
-    if (false)
-#endif
-      sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0],
-                     NPASS == 1 ? kBDelta1 : kBDeltaN, &b0, &b1, &b2, &b3, &b4);
+    if (h ? act[1] : act[0]) {
+      if (CONT) {
+        const int64_t k = h ? kk[1] : kk[0];
+        const float2 r = P.NEXTr[(P.seeds ? P.seeds[k] : k) * m + j];
+        b0 = b3 = r.x;
+        b1 = b4 = r.y;
+        b2 = 0.5f * (r.x + r.y);
+      } else {
+        sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0], P.delta, &b0,
+                       &b1, &b2, &b3, &b4);
+      }
+    }
     float* d = &sbr[half][0][slot];
     d[0] = b0;
     d[kBSlots] = b1;
@@ -323,11 +354,10 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     d[4 * kBSlots] = b4;
   }
   const int64_t nch = (n + kBRows - 1) / kBRows;
-  const int64_t nseq = NPASS * nch;  // chunks consumed over all passes, in order
-  // stage refill: the chunk with sequence number g goes to stage g % kBStages
-  auto issue = [&](int64_t g) {
-    const int st = (int)(g % kBStages);
-    const int64_t i0 = (g % nch) * kBRows;
+  // stage refill: chunk c goes to stage c % kBStages
+  auto issue = [&](int64_t c) {
+    const int st = (int)(c % kBStages);
+    const int64_t i0 = c * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
     fence_proxy_async();
     mbar_expect_tx(&full[st], (unsigned)kBStage);
@@ -341,166 +371,95 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
       done[s] = 0u;
     }
     mbar_fence_init();
-    for (int64_t g = 0; g < min((int64_t)kBStages, nseq); ++g) issue(g);
+    for (int64_t c = 0; c < min((int64_t)kBStages, nch); ++c) issue(c);
   }
+  // this thread's share of the histograms (problem `half`)
+#pragma unroll
+  for (int b = 0; b < kNB; ++b) hist[(half * kNB + b) * kBSlots + slot] = 0u;
   __syncthreads();
+  float lo[2], hi[2], cf[2], A[2], B[2];
+  unsigned hb[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     lo[t] = sbr[t][0][slot];
     hi[t] = sbr[t][1][slot];
-    cen[t] = sbr[t][2][slot];
-    smin[t] = sbr[t][3][slot];
-    smax[t] = sbr[t][4][slot];
+    cf[t] = sbr[t][2][slot];
+    A[t] = (62.f / 63.f) / (hi[t] - lo[t]);
+    B[t] = 0.5f / 63.f - lo[t] * A[t];
+    hb[t] = smem_u32(hist + t * kNB * kBSlots + slot) - 0x4B000000u * (unsigned)(kBSlots * 4);
   }
 
   unsigned fphase = 0;
   const bool busy = __any_sync(0xffffffffu, act[0] || act[1]);
-  int64_t consumed = 0;  // chunks consumed over all passes
-  double ec0 = 0.0, ec1 = 0.0;  // this half's share of e_j(c) of both problems (last pass)
-  float cf[2];
-  for (int pass = 0; pass < NPASS; ++pass) {
-    const bool resid = pass == NPASS - 1;
-    float A[2], B[2];
-    unsigned hb[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      A[t] = (62.f / 63.f) / (hi[t] - lo[t]);
-      B[t] = 0.5f / 63.f - lo[t] * A[t];
-      cf[t] = pass == 0 ? cen[t] : 0.5f * (lo[t] + hi[t]);
-      if (half == t) {
-#pragma unroll
-        for (int b = 0; b < kNB; ++b) hist[(t * kNB + b) * kBSlots + slot] = 0u;
-      }
-      hb[t] = smem_u32(hist + t * kNB * kBSlots + slot) - 0x4B000000u * (unsigned)(kBSlots * 4);
-    }
-    __syncthreads();
-    const int64_t c0 = consumed;
-    for (int64_t c = 0; c < nch; ++c) {
-      const int st = (int)((c0 + c) % kBStages);
-      mbar_wait(&full[st], (fphase >> st) & 1u);
-      fphase ^= 1u << st;
-#ifndef KB_NOCOMPUTE
-      if (busy) {
-#else
-      if (false) {
-#endif
-        const unsigned char* sb = smem + (size_t)st * kBStage;
-        const float* ta = (const float*)sb;
-        const float4* pf4 = (const float4*)(sb + kBTile) + pair;  // (y, x_ip) of pivots 2w', 2w'+1
-        const uint2* pu2 = (const uint2*)(sb + kBTile + kBPlane) + pair;  // their 32-bit weights
-        float r0acc = 0.f, r1acc = 0.f;
+  double ec0 = 0.0, ec1 = 0.0;  // this half's share of e_j(c) of both problems
+  for (int64_t c = 0; c < nch; ++c) {
+    const int st = (int)(c % kBStages);
+    mbar_wait(&full[st], (fphase >> st) & 1u);
+    fphase ^= 1u << st;
+    if (busy) {
+      const unsigned char* sb = smem + (size_t)st * kBStage;
+      const float* ta = (const float*)sb;
+      const float4* pf4 = (const float4*)(sb + kBTile) + pair;  // (y, x_ip) of pivots 2w', 2w'+1
+      const uint2* pu2 = (const uint2*)(sb + kBTile + kBPlane) + pair;  // their 32-bit weights
+      float r0acc = 0.f, r1acc = 0.f;
 #pragma unroll kBUnroll
-        for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
-          float av[4];
-          float4 yw[4];
-          uint2 wu[4];
+      for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
+        float av[4];
+        float4 yw[4];
+        uint2 wu[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            av[u] = ta[(r0 + u) * 32 + lane];
-            yw[u] = pf4[(r0 + u) * 4];
-            wu[u] = pu2[(r0 + u) * 4];
-          }
-          unsigned a0[4], a1[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float q0 = av[u] * yw[u].x, q1 = av[u] * yw[u].z;
-            a0[u] = hb[0] + __float_as_uint(fmaf(__saturatef(fmaf(q0, A[0], B[0])), 63.f, 8388608.f)) *
-                                (unsigned)(kBSlots * 4);
-            a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
-                                (unsigned)(kBSlots * 4);
-          }
-#ifndef KB_NORESID
-          if (resid) {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
-            float e0[4], e1[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              e0[u] = fabsf(fmaf(-cf[0], yw[u].y, av[u]));
-              e1[u] = fabsf(fmaf(-cf[1], yw[u].w, av[u]));
-            }
-            r0acc += (e0[0] + e0[1]) + (e0[2] + e0[3]);
-            r1acc += (e1[0] + e1[1]) + (e1[2] + e1[3]);
-          }
-#endif
-          // fire-and-forget shared adds (the other half adds into the same bins)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-#ifndef KB_NOATOM
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[u]), "r"(wu[u].x));
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[u]), "r"(wu[u].y));
-#else
-            r0acc += __uint_as_float(a0[u] ^ wu[u].x);
-            r1acc += __uint_as_float(a1[u] ^ wu[u].y);
-#endif
-          }
+        for (int u = 0; u < 4; ++u) {
+          av[u] = ta[(r0 + u) * 32 + lane];
+          yw[u] = pf4[(r0 + u) * 4];
+          wu[u] = pu2[(r0 + u) * 4];
         }
-        if (resid) {
-          ec0 += (double)r0acc;
-          ec1 += (double)r1acc;
+        unsigned a0[4], a1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float q0 = av[u] * yw[u].x, q1 = av[u] * yw[u].z;
+          a0[u] = hb[0] + __float_as_uint(fmaf(__saturatef(fmaf(q0, A[0], B[0])), 63.f, 8388608.f)) *
+                              (unsigned)(kBSlots * 4);
+          a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
+                              (unsigned)(kBSlots * 4);
+        }
+        {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
+          float e0[4], e1[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            e0[u] = fabsf(fmaf(-cf[0], yw[u].y, av[u]));
+            e1[u] = fabsf(fmaf(-cf[1], yw[u].w, av[u]));
+          }
+          r0acc += (e0[0] + e0[1]) + (e0[2] + e0[3]);
+          r1acc += (e1[0] + e1[1]) + (e1[2] + e1[3]);
+        }
+        // fire-and-forget shared adds (the other half adds into the same bins)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[u]), "r"(wu[u].x));
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[u]), "r"(wu[u].y));
         }
       }
-      __syncwarp();
-      if (lane == 0) {
-        // the last warp done with the stage refills it (no producer waits)
-        unsigned old;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                     : "=r"(old)
-                     : "r"(smem_u32(&done[st]))
-                     : "memory");
-        if (old == kBWarps - 1) {
-          done[st] = 0u;
-          const int64_t g = c0 + c + kBStages;
-          if (g < nseq) issue(g);
-        }
-      }
+      ec0 += (double)r0acc;
+      ec1 += (double)r1acc;
     }
-    consumed += nch;
-    __syncthreads();  // both halves' adds are in
-    if (pass + 1 < NPASS) {
-      // next range: the edges between which the optimum provably lies (last
-      // edge with g <= 0, first with g >= 0, histogram margins included, as
-      // column_bounds uses them), a little wider; when one side is not in
-      // the bracket the optimum lies beyond it and the range extends there.
-      // Both halves compute it (same inputs, same result).
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (!act[t]) continue;
-        const double T = Tq[t] * unit[t], lam = P.lam, w = ((double)hi[t] - (double)lo[t]) / (double)kNI;
-        const double q = ldexp(unit[t], 21), dC = 0.5000001 * (double)n * q;
-        double C = 0.0;
-        int kL = -1, kR = -1;
-        for (int k = 0; k <= kNI; ++k) {
-          C += (double)hist[(t * kNB + k) * kBSlots + slot] * q;
-          const double e = (double)lo[t] + (double)k * w;
-          if (2.0 * (C + dC) - T + (e > 0.0 ? lam : -lam) <= 0.0) kL = k;
-          if (2.0 * (C - dC) - T + (e >= 0.0 ? lam : -lam) >= 0.0) { kR = k; break; }
-        }
-        const float span = hi[t] - lo[t];
-        float a, b;
-        if (kL >= 0 && kR >= 0) {
-          a = (float)((double)lo[t] + (double)max(0, min(kL, kR - 1)) * w);
-          b = (float)((double)lo[t] + (double)min(kNI, max(kR, kL + 1)) * w);
-        } else if (kR >= 0) {  // optimum at or below lo: extend down
-          a = fminf(smin[t], lo[t]) - 2.f * span;
-          b = (float)((double)lo[t] + (double)kR * w);
-        } else if (kL >= 0) {  // at or above the last edge: extend up
-          a = (float)((double)lo[t] + (double)kL * w);
-          b = fmaxf(smax[t], hi[t]) + 2.f * span;
-        } else {  // no edge is decisive (margins dominate): keep the range
-          a = lo[t];
-          b = hi[t];
-        }
-        const float mg = 0.05f * (b - a);
-        lo[t] = a - mg;
-        hi[t] = b + mg;
-        if (!(hi[t] > lo[t])) hi[t] = lo[t] + fmaxf(fabsf(lo[t]), 1e-30f) * 1e-6f;
+    __syncwarp();
+    if (lane == 0) {
+      // the last warp done with the stage refills it (no producer waits)
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "r"(smem_u32(&done[st]))
+                   : "memory");
+      if (old == kBWarps - 1) {
+        done[st] = 0u;
+        if (c + kBStages < nch) issue(c + kBStages);
       }
-      __syncthreads();  // histograms read before the next pass clears them
     }
   }
   // half 1 finishes problem 1 with half 0's share of its residual, half 0
   // problem 0 with half 1's share
   if (half == 1) sec[slot] = ec0;
-  __syncthreads();
+  __syncthreads();  // also: both halves' histogram adds are in
   const double ec = half == 0 ? ec0 + sec[slot] : 0.0;
   __syncthreads();
   if (half == 0) sec[slot] = ec1;
@@ -510,20 +469,20 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   if (j >= m || !(h ? ok[1] : ok[0])) return;
   const int64_t o = (h ? kk[1] : kk[0]) * m + j;
   const bool dg = h ? degen[1] : degen[0];
+  const float tlo = h ? lo[1] : lo[0], thi = h ? hi[1] : hi[0];
   if (dg || j == (h ? p[1] : p[0])) {
     const double z = dg ? P.colsum[j] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
     P.LB[o] = z;
     P.UB[o] = z;
     P.BRK[o] = make_double2(-INFINITY, INFINITY);
+    P.NEXTw[o] = make_float2(tlo, thi);
     return;
   }
   const double ut = h ? unit[1] : unit[0];
-  double lb = 0.0, ub = 0.0;
-#ifndef KB_NOEPI
-  column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
-                (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam,
-                P.colsum[j], n, &lb, &ub, &P.BRK[o]);
-#endif
+  double lb, ub;
+  column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)tlo, (double)thi,
+                (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam, P.colsum[j], n,
+                sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
 }

@@ -77,7 +77,10 @@ struct SelParams {
   double* LB;            // bound mode: [npiv][m] lower / upper bound of each column's optimum
   double* UB;
   double2* BRK;          // bound mode: [npiv][m] range holding each column's optimum v
-  const int64_t* seeds;  // seeded fit: row of BRK (bound-call pivot position) per pivot, -1 none
+  const int64_t* seeds;  // seeded fit / continued bound: position in the previous bound call's list
+  const float2* NEXTr;   // bound mode: ranges the previous pass left ([npiv][m])
+  float2* NEXTw;         // bound mode: ranges this pass leaves
+  int delta;             // bound mode: sample bracket half-width (ranks)
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {

@@ -37,9 +37,9 @@ RESCORE_ATOL = 1e-13
 # upper bound (the bounds already carry their float-error margins; this
 # covers the reference's own rounding of the objective)
 PRUNE_RTOL = 1e-9
-# refine (multi-pass bounds on the survivors) when the one-pass bounds keep
-# more than this many pivots; three passes cost ~3 one-pass bounds per pivot
-# (a quarter of an exact fit or less) and leave one or a few candidates
+# refine (one more bounding pass per level on the survivors) while more than
+# REFINE_MIN pivots survive, at most REFINE_PASSES levels; each level costs
+# one pass per surviving pivot and shrinks the bound gaps ~1000x
 REFINE_MIN = 2
 REFINE_PASSES = 3
 
@@ -266,6 +266,20 @@ class DeviceFit:
                        "l1b_bound_columns")
         return lb, ub
 
+    def bound_pivot_list_continue(self, lam: float, pivots, from_pos, from_npiv: int):
+        """One more bounding pass for pivots[k] = entry from_pos[k] of the last bound call's list."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        fp = np.ascontiguousarray(np.asarray(from_pos, dtype=np.int64))
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, piv.size), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_pivot_list_continue(
+                self.X.data_ptr(), self.n, self.m, float(lam), piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                piv.size, fp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(from_npiv), b[0].data_ptr(),
+                b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+            _lib.check(rc, "l1b_bound_pivot_list_continue")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
     def _winner(self, lam: float, pivots, V, obj_h) -> PivotWinner:
         """fit.py:98-102 among fitted pivots: re-score the near-minimal ones
         with the reference's rounding, first strict minimum wins."""
@@ -333,11 +347,13 @@ class DeviceFit:
                 out.append(None)
                 continue
             seed, seed_n = keep, npiv  # positions in the last bound call's pivot list
-            if keep.size > REFINE_MIN:
-                # second stage on the survivors: every further pass
-                # re-histograms the range holding the optimum, so the bounds
-                # tighten by orders of magnitude; cheaper than exact fits
-                lb2, ub2 = self.bound_pivot_list(float(lam[l]), all_piv[keep], passes=REFINE_PASSES)
+            for _ in range(REFINE_PASSES):
+                if keep.size <= REFINE_MIN:
+                    break
+                # refine the survivors: one more pass each, over the range
+                # where the last pass proved each column's optimum lies, so
+                # the bounds tighten by orders of magnitude per level
+                lb2, ub2 = self.bound_pivot_list_continue(float(lam[l]), all_piv[keep], seed, seed_n)
                 top = min(top, float(np.min(ub2)))
                 sel = np.nonzero(~(lb2 > self._prune_threshold(top)))[0]
                 keep, seed, seed_n = keep[sel], sel, keep.size

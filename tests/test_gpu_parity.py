@@ -348,10 +348,15 @@ def _bounds_hold(X, lam):
         np.fill_diagonal(lbc, 0.0)
         np.fill_diagonal(ubc, 0.0)
         assert np.all(lbc <= F + ftol) and np.all(F <= ubc + ftol), lam
-    # the multi-pass refinement on a pivot list (every other pivot, reversed)
+    # the multi-pass refinement on a pivot list (every other pivot, reversed),
+    # and the cascade: one more pass continuing from the all-pivot pass above
     piv = np.arange(X.shape[1])[::-2].copy()
-    for passes in (2, 3):
-        lb2, ub2 = eng.bound_pivot_list(lam, piv, passes=passes)
+    for passes in (2, 3, "continue"):
+        if passes == "continue":
+            eng.bound_pivots(lam)
+            lb2, ub2 = eng.bound_pivot_list_continue(lam, piv, piv, X.shape[1])
+        else:
+            lb2, ub2 = eng.bound_pivot_list(lam, piv, passes=passes)
         assert np.all(lb2 <= o[piv] + tol[piv]), (lam, passes, np.max(lb2 - o[piv]))
         assert np.all(o[piv] <= ub2 + tol[piv]), (lam, passes, np.max(o[piv] - ub2))
         if not cols:
