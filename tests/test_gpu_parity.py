@@ -56,7 +56,8 @@ def _pivots(X, lams, **kw):
     return eng, V.cpu().numpy(), E.cpu().numpy(), P.cpu().numpy(), O.cpu().numpy()
 
 
-@pytest.mark.parametrize("n,m", [(1, 3), (37, 11), (3000, 7001), (100000, 500)])
+@pytest.mark.parametrize("n,m", [(1, 3), (2, 3), (37, 11), (61, 7), (129, 5), (300, 17), (2000, 2000), (3000, 7001),
+                                 (100000, 500)])
 def test_residual_exact_matches_numpy_bits(n, m):
     """l1b_residual_exact == residual_error (core.py:93) bit for bit, up to C4's n*m."""
     rng = np.random.default_rng(n + m)
