@@ -399,6 +399,14 @@ def run_ours(args):
                                         "8 in flight per thread)",
                          "fp32_view": {"ops_per_element": 5, "achieved_TOPs": 5 * kb_rate / 1e12,
                                        "peak_TOPs": _fp32_peak(dev) / 1e12},
+                         "step_view": {
+                             "note": "whole pruned step against the exact algorithm's FP64 floor (SURVEY.md 8d: "
+                                     "11 FP64 ops per ratio element, E = n*m*(m-1) per fit); > 1 means the step "
+                                     "beats that floor by skipping provably losing pivots",
+                             "elements_per_step": elems * ncomp,
+                             "achieved_elements_per_s": elems * ncomp / (ms_total / args.steps / 1e3),
+                             "exact_fp64_floor_elements_per_s": fp64_ops / 11.0,
+                             "frac": elems * ncomp / (ms_total / args.steps / 1e3) / (fp64_ops / 11.0)},
                          "exact_fit_view": {
                              "kernel": "k_select+k_resolve+k_straggle (exact fit of every pivot)",
                              "achieved": achieved / 1e12, "peak": fp64_ops / 1e12,
