@@ -1060,3 +1060,195 @@ __global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
     __syncwarp();
   }
 }
+
+// ------------------------------------------------ block-per-problem solver --
+//
+// The seeded exact fit of a few candidate pivots over tall data (n large):
+// k_straggle's rounds with a whole CTA per problem, rows strided over its
+// 256 threads, so few problems still fill the GPU.  Each round visits every
+// row once: exact weight below the key interval, Wneg on the first round
+// (for G), and the interval's elements collected into shared memory; if they
+// fit (<= kBlkCap) they are bitonic-sorted by (key, row) and walked in order,
+// else a second visit narrows the interval by a 256-bucket exact histogram.
+// Starts on the range the bound cascade left (P.BRK row P.seeds[k]).
+
+constexpr int kBlkThreads = 256;
+constexpr int kBlkCap = 2048;
+constexpr size_t kBlkSmem = (size_t)kBlkCap * sizeof(SEnt) + kSBins * sizeof(unsigned long long);
+
+__device__ __forceinline__ double block_sum(double x, double* red) {
+  x = warp_sum(x);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red is reused
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double t = 0.0;
+  for (int k = 0; k < kBlkThreads / 32; ++k) t += red[k];  // fixed order, every thread
+  return t;
+}
+
+template <bool SAFE>
+__global__ void __launch_bounds__(kBlkThreads) k_block_solve(SelParams P) {
+  extern __shared__ __align__(16) unsigned char bsm[];
+  SEnt* ent = reinterpret_cast<SEnt*>(bsm);
+  unsigned long long* bins = reinterpret_cast<unsigned long long*>(bsm + (size_t)kBlkCap * sizeof(SEnt));
+  __shared__ double red[kBlkThreads / 32];
+  __shared__ int cnt_s;
+  const int tid = threadIdx.x;
+  const int64_t n = P.n, m = P.m;
+  for (int64_t prob = blockIdx.x; prob < P.npiv * m; prob += gridDim.x) {
+    const int64_t kk = prob / m, j = prob - kk * m, p = pivot_of(P, kk);
+    if (P.nnz[p] == 0 || j == p) {  // degenerate pivot / the pivot's own column
+      if (tid == 0) {
+        P.V[prob] = P.nnz[p] == 0 ? 0.0 : 1.0;
+        P.E[prob] = P.nnz[p] == 0 ? P.colsum[j] : 0.0;
+      }
+      continue;
+    }
+    const double Tq = P.tq[p], Lsc = ldexp(P.lam, P.spow[p]);
+    unsigned long long lo = 0, hi = ~0ULL;
+    const int64_t sr = P.seeds ? P.seeds[kk] : -1;
+    if (sr >= 0) {
+      const double2 r = P.BRK[sr * m + j];
+      if (r.x > -INFINITY && r.y < INFINITY && r.x <= r.y) {
+        lo = key64(r.x - fabs(r.x) * 0x1p-18 - 0x1p-1000);
+        hi = key64(r.y + fabs(r.y) * 0x1p-18 + 0x1p-1000);
+      }
+    }
+    const double* xc = P.Xc + j * n;
+    const double* pb = P.pb + p * P.np;
+    const double* py = P.py + p * P.np;
+    const double* pw = P.pw + p * P.np;
+    auto row_key = [&](int64_t i, double* w) -> unsigned long long {
+      *w = pw[i];
+      return key64(sratio<SAFE>(P, xc[i], pb[i], py[i]));
+    };
+    double G = -1.0, v = 0.0;
+    bool ok = false;
+    for (int round = 0; round < 64 && !ok; ++round) {
+      const bool needG = G < 0.0;
+      if (tid == 0) cnt_s = 0;
+      __syncthreads();
+      double wbl = 0.0, wneg = 0.0;
+      for (int64_t i = tid; i < n; i += kBlkThreads) {
+        double w;
+        const unsigned long long k = row_key(i, &w);
+        if (w == 0.0) continue;  // x_ip = 0: not in the tableau (ratios.py:115)
+        if (k < lo) wbl += w;
+        if (needG && k < kZeroKey) wneg += w;
+        if (k >= lo && k <= hi) {
+          const int pos = atomicAdd(&cnt_s, 1);
+          if (pos < kBlkCap) ent[pos] = SEnt{k, w, (int)i, 0};
+        }
+      }
+      wbl = block_sum(wbl, red);
+      if (needG) {
+        wneg = block_sum(wneg, red);
+        if (!region_G(Tq, wneg, Lsc, &G)) {  // dead: v = +0.0
+          v = 0.0;
+          ok = true;
+          break;
+        }
+      }
+      const int cnt = cnt_s;
+      if (G < wbl) {  // the crossing lies below the interval
+        hi = lo - 1;
+        lo = 0;
+        continue;
+      }
+      if (cnt <= kBlkCap) {
+        int np2 = 1;
+        while (np2 < cnt) np2 <<= 1;
+        for (int e = cnt + tid; e < np2; e += kBlkThreads) ent[e] = SEnt{~0ULL, 0.0, 0x7fffffff, 0};
+        __syncthreads();
+        for (int kq = 2; kq <= np2; kq <<= 1) {
+          for (int jq = kq >> 1; jq > 0; jq >>= 1) {
+            for (int e = tid; e < np2; e += kBlkThreads) {
+              const int l = e ^ jq;
+              if (l > e) {
+                const SEnt a = ent[e], b = ent[l];
+                const bool gt = a.k > b.k || (a.k == b.k && a.row > b.row);
+                if (gt == ((e & kq) == 0)) {
+                  ent[e] = b;
+                  ent[l] = a;
+                }
+              }
+            }
+            __syncthreads();
+          }
+        }
+        // in-order walk (warp 0): the first element whose prefix exceeds G
+        int hit = -1;
+        if (tid < 32) {
+          double cum = wbl;
+          for (int e0 = 0; e0 < cnt && hit < 0; e0 += 32) {
+            const int e = e0 + tid;
+            double x = e < cnt ? ent[e].w : 0.0;
+            for (int o = 1; o < 32; o <<= 1) {
+              const double y = __shfl_up_sync(0xffffffffu, x, o);
+              if (tid >= o) x += y;
+            }
+            const unsigned cm = __ballot_sync(0xffffffffu, e < cnt && cum + x > G);
+            if (cm) hit = e0 + __ffs(cm) - 1;
+            cum += __shfl_sync(0xffffffffu, x, 31);
+          }
+          if (tid == 0) cnt_s = hit;
+        }
+        __syncthreads();
+        hit = cnt_s;
+        if (hit >= 0) {
+          const SEnt h = ent[hit];
+          v = h.k == kZeroKey ? __ddiv_rn(xc[h.row], pb[h.row]) : key64_inv(h.k);
+          ok = true;
+        } else {  // the crossing lies above the interval
+          if (hi == ~0ULL) break;
+          lo = hi + 1;
+          hi = ~0ULL;
+        }
+        __syncthreads();
+      } else {
+        // narrow: exact weight per key bucket, then the crossing bucket
+        int sh = (hi - lo == ~0ULL) ? 56 : ceil_log2_u64(hi - lo + 1) - 8;
+        sh = sh > 0 ? sh : 0;
+        for (int b = tid; b < kSBins; b += kBlkThreads) bins[b] = 0ULL;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += kBlkThreads) {
+          double w;
+          const unsigned long long k = row_key(i, &w);
+          if (w != 0.0 && k >= lo && k <= hi) atomicAdd(&bins[(k - lo) >> sh], (unsigned long long)w);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double cum = wbl;
+          int bsel = kSBins - 1;
+          for (int b = 0; b < kSBins; ++b) {
+            const double hb = (double)bins[b];
+            if (cum + hb > G) { bsel = b; break; }
+            cum += hb;
+          }
+          red[0] = __longlong_as_double((long long)bsel);
+        }
+        __syncthreads();
+        const int bsel = (int)__double_as_longlong(red[0]);
+        const unsigned long long nlo = lo + ((unsigned long long)bsel << sh);
+        unsigned long long nhi = nlo + ((1ULL << sh) - 1);
+        if (nhi > hi || nhi < nlo) nhi = hi;
+        lo = nlo;
+        hi = nhi;
+        __syncthreads();
+      }
+    }
+    if (!ok) {
+      if (tid == 0) atomicExch(P.status, L1B_EINTERNAL);
+      v = 0.0;
+    }
+    double e = 0.0;
+    for (int64_t i = tid; i < n; i += kBlkThreads) e += fabs(__dsub_rn(xc[i], __dmul_rn(pb[i], v)));
+    e = block_sum(e, red);
+    if (tid == 0) {
+      P.V[prob] = v;
+      P.E[prob] = e;
+    }
+    __syncthreads();
+  }
+}
