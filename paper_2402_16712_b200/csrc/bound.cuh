@@ -303,7 +303,11 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 // and target (lane) and split each chunk's rows (alternate 4-row groups);
 // both add into the problem's one histogram with shared-memory atomics, so
 // the CTA holds 8 warps for the histogram space of 4.
-template <bool CONT>
+// SPLIT (few pivots, many rows: a grid too small to fill the GPU): the rows
+// are also split over blockIdx.z; every CTA adds its histograms into P.GH
+// (exact integer sums, any order), leaves its residual share in P.GE[z] and
+// (z = 0) the ranges in P.GB, and k_bound_epi finishes each problem.
+template <bool CONT, bool SPLIT>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
@@ -353,11 +357,13 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     d[3 * kBSlots] = b3;
     d[4 * kBSlots] = b4;
   }
-  const int64_t nch = (n + kBRows - 1) / kBRows;
-  // stage refill: chunk c goes to stage c % kBStages
+  const int64_t nall = (n + kBRows - 1) / kBRows;
+  const int64_t cb = SPLIT ? nall * blockIdx.z / gridDim.z : 0;  // this CTA's chunks [cb, cb + nch)
+  const int64_t nch = SPLIT ? nall * (blockIdx.z + 1) / gridDim.z - cb : nall;
+  // stage refill: local chunk c (global cb + c) goes to stage c % kBStages
   auto issue = [&](int64_t c) {
     const int st = (int)(c % kBStages);
-    const int64_t i0 = c * kBRows;
+    const int64_t i0 = (cb + c) * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
     fence_proxy_async();
     mbar_expect_tx(&full[st], (unsigned)kBStage);
@@ -468,6 +474,23 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   const double ect = h ? ec1 + sec[slot] : ec;
   if (j >= m || !(h ? ok[1] : ok[0])) return;
   const int64_t o = (h ? kk[1] : kk[0]) * m + j;
+  if (SPLIT) {
+    const unsigned* hc = hist + half * kNB * kBSlots + slot;
+    for (int b = 0; b < kNB; ++b) {
+      const unsigned x = hc[b * kBSlots];
+      if (x) atomicAdd(&P.GH[o * kNB + b], x);
+    }
+    P.GE[(int64_t)blockIdx.z * P.npiv * m + o] = ect;
+    if (blockIdx.z == 0) {
+      float* g = P.GB + o * 5;
+      g[0] = h ? lo[1] : lo[0];
+      g[1] = h ? hi[1] : hi[0];
+      g[2] = h ? cf[1] : cf[0];
+      g[3] = sbr[half][3][slot];
+      g[4] = sbr[half][4][slot];
+    }
+    return;
+  }
   const bool dg = h ? degen[1] : degen[0];
   const float tlo = h ? lo[1] : lo[0], thi = h ? hi[1] : hi[0];
   if (dg || j == (h ? p[1] : p[0])) {
@@ -483,6 +506,32 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)tlo, (double)thi,
                 (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam, P.colsum[j], n,
                 sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
+  P.LB[o] = lb;
+  P.UB[o] = ub;
+}
+
+// Epilogue of a SPLIT k_bound: thread per (pivot, target) problem, the
+// merged histogram, the residual shares summed in z order, column_bounds.
+__global__ void k_bound_epi(SelParams P, int nsplit) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t m = P.m;
+  if (o >= P.npiv * m) return;
+  const int64_t kk = o / m, j = o - kk * m, p = pivot_of(P, kk);
+  const float* g = P.GB + o * 5;
+  if (P.nnz[p] == 0 || j == p) {
+    const double z = P.nnz[p] == 0 ? P.colsum[j] : 0.0;
+    P.LB[o] = z;
+    P.UB[o] = z;
+    P.BRK[o] = make_double2(-INFINITY, INFINITY);
+    P.NEXTw[o] = make_float2(g[0], g[1]);
+    return;
+  }
+  double ec = 0.0;
+  for (int z = 0; z < nsplit; ++z) ec += P.GE[(int64_t)z * P.npiv * m + o];
+  const double ut = ldexp(1.0, -P.spow[p]);
+  double lb, ub;
+  column_bounds(P.GH + o * kNB, 1, ldexp(ut, 21), (double)g[0], (double)g[1], (double)g[2], ec, P.tq[p] * ut,
+                P.lam, P.colsum[j], P.n, g[3], g[4], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
 }

@@ -81,6 +81,9 @@ struct SelParams {
   const float2* NEXTr;   // bound mode: ranges the previous pass left ([npiv][m])
   float2* NEXTw;         // bound mode: ranges this pass leaves
   int delta;             // bound mode: sample bracket half-width (ranks)
+  unsigned* GH;          // split bound: merged histograms [npiv*m][64]
+  double* GE;            // split bound: residual shares [z][npiv*m]
+  float* GB;             // split bound: ranges [npiv*m][5]
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {
