@@ -148,8 +148,11 @@ __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double 
   auto f_hi = [&](int k, long long SC, long long Cu) {
     return k >= kc ? fkc_hi + (Ihi(k, SC, Cu) - IhiC) : fkc_hi - (IloC - Ilo(k, SC));
   };
-  const double f0 = colsum;  // f(0): the dead value, exact
-  double lb, ub = fmin(fc + eps, f0);
+  // f(0) = sum_i |x_ij|: the dead value; colsum carries the rounding of an
+  // n-term f64 sum (any order): within (n + 128) 2^-53 of it
+  const double f0e = (double)(n + 128) * 0x1p-53 * colsum;
+  const double f0 = colsum - f0e;  // a lower bound of f(0) (the kink bounds below)
+  double lb, ub = fmin(fc + eps, colsum + f0e);
   const double eL = kL >= 0 ? edge(kL) : -INFINITY, eR = kR <= kNI ? edge(kR) : INFINITY;
   if (kL >= 0 && kR <= kNI && kL <= kR) {
     lb = f_lo(kL, SCL, CuL) - eps + fmin(0.0, gloL) * (eR - eL);
