@@ -43,9 +43,8 @@ constexpr int kBSlots = kBPairs * 32;      // histogram columns: (pair, target)
 #endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
 constexpr int kBTile = kBRows * 32 * 4;    // x_ij float tile [row][32 targets]
-constexpr int kBPlane = kBRows * kWarps * 8;   // (y32, x_ip32) [row][8 pivots]
-constexpr int kBPlaneU = kBRows * kWarps * 4;  // 32-bit weights [row][8 pivots]
-constexpr int kBStage = kBTile + kBPlane + kBPlaneU;
+constexpr int kBPlane = kBRows * kWarps * 12;  // k_group_bound records: 12 B per (row, pivot)
+constexpr int kBStage = kBTile + kBPlane;
 constexpr int kBStages = KB_STAGES;
 constexpr int kBUnroll = KB_UNROLL;        // 8-row groups per main-loop iteration
 constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [problem][bin][slot], exact 32-bit sums
@@ -371,8 +370,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     fence_proxy_async();
     mbar_expect_tx(&full[st], (unsigned)kBStage);
     bulk_g2s(base, P.Xft + tbase + i0 * 32, kBTile, &full[st]);
-    bulk_g2s(base + kBTile, P.gpf + gbase + i0 * 8, kBPlane, &full[st]);
-    bulk_g2s(base + kBTile + kBPlane, P.gwu + gbase + i0 * 8, kBPlaneU, &full[st]);
+    bulk_g2s(base + kBTile, P.gbp + (gbase + i0 * 8) * 3 / 4, kBPlane, &full[st]);
   };
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
@@ -408,19 +406,24 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     if (busy) {
       const unsigned char* sb = smem + (size_t)st * kBStage;
       const float* ta = (const float*)sb;
-      const float4* pf4 = (const float4*)(sb + kBTile) + pair;  // (y, x_ip) of pivots 2w', 2w'+1
-      const uint2* pu2 = (const uint2*)(sb + kBTile + kBPlane) + pair;  // their 32-bit weights
+      // records of this warp's pivot pair: 3 float4 per row pair, 4 pairs per row pair
+      const float4* rec = (const float4*)(sb + kBTile) + pair * 3;
       float r0acc = 0.f, r1acc = 0.f;
 #pragma unroll kBUnroll
       for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
         float av[4];
-        float4 yw[4];
+        float4 yw[4];  // (y0, x0, y1, x1) of row r0 + u, as the old plane had it
         uint2 wu[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          av[u] = ta[(r0 + u) * 32 + lane];
-          yw[u] = pf4[(r0 + u) * 4];
-          wu[u] = pu2[(r0 + u) * 4];
+        for (int u = 0; u < 4; ++u) av[u] = ta[(r0 + u) * 32 + lane];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {  // row pairs (r0, r0+1), (r0+2, r0+3)
+          const float4* rp = rec + ((r0 >> 1) + h2) * 12;
+          const float4 L0 = rp[0], L1 = rp[1], L2 = rp[2];
+          yw[2 * h2] = make_float4(L0.x, L0.z, L0.y, L0.w);
+          wu[2 * h2] = make_uint2(__float_as_uint(L1.x), __float_as_uint(L1.y));
+          yw[2 * h2 + 1] = make_float4(L1.z, L2.x, L1.w, L2.y);
+          wu[2 * h2 + 1] = make_uint2(__float_as_uint(L2.z), __float_as_uint(L2.w));
         }
         unsigned a0[4], a1[4];
 #pragma unroll

@@ -46,6 +46,7 @@ struct SelParams {
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
   const unsigned* gwu;   // shard wq_ip / 2^21 (rounded) in 8-pivot groups
+  const float4* gbp;     // k_bound plane (see k_group_bound)
   const double* Xc;      // column-major m x n
   const double* pb;      // [m][n] x_ip
   const double* py;      // [m][n] hoisted reciprocal (NaN: dropped row)
