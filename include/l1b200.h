@@ -84,6 +84,15 @@ int l1b_fit_pivot_list(const double* d_X, int64_t n, int64_t m, const double* h_
 int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
                      int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
+/* l1b_bound_pivots for nlam penalties (strictly ascending, host memory) in
+ * ONE pass: the histogram range covers the crossings of the smallest and
+ * largest penalty (and 0 where the largest may kill the column), and every
+ * penalty gets its own bounds from the same histogram and residual.
+ * d_lb / d_ub are [nlam][npiv] (device).  The batched lambda sweep (C3). */
+int l1b_bound_pivots_multi(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam,
+                           int64_t p_begin, int64_t p_stride, int64_t npiv, double* d_lb, double* d_ub, void* d_ws,
+                           size_t ws_bytes, void* stream);
+
 /* l1b_bound_pivots for a pivot list (host memory) with 1 to 3 passes per
  * problem: every further pass re-histograms the range where the previous
  * one proved the optimum lies (62 sub-bins; or extends the range when the

@@ -37,6 +37,7 @@ ABI_SYMBOLS = (
     "l1b_bound_columns",
     "l1b_fit_pivot_list_seeded",
     "l1b_bound_pivot_list_continue",
+    "l1b_bound_pivots_multi",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -116,6 +117,9 @@ def load() -> ctypes.CDLL:
     lib.l1b_bound_pivot_list_continue.restype = ctypes.c_int
     lib.l1b_bound_pivot_list_continue.argtypes = [_vp, _i64, _i64, ctypes.c_double, _vp, _i64, _vp, _i64, _vp,
                                                   _vp, _vp, _sz, _vp]
+    lib.l1b_bound_pivots_multi.restype = ctypes.c_int
+    lib.l1b_bound_pivots_multi.argtypes = [_vp, _i64, _i64, _vp, ctypes.c_int32, _i64, _i64, _i64, _vp, _vp, _vp,
+                                           _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

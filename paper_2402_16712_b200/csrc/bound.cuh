@@ -217,9 +217,11 @@ __device__ __forceinline__ float key2f(unsigned k) {
   return __uint_as_float(k ^ (((unsigned)((int)~k >> 31)) | 0x80000000u));
 }
 
+// lam_lo < lam_hi (one pass for several penalties): the bracket covers the
+// estimated crossings of both, and 0 when lam_hi may kill the column.
 __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
                                                double unit, int delta, float* lo, float* hi, float* cen,
-                                               float* smin, float* smax) {
+                                               float* smin, float* smax, double lam_lo, double lam_hi) {
   const int64_t n = P.n;
   float sr[kSample], sw[kSample];
   float wmax = 0.f;
@@ -258,19 +260,25 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
     ws += wq;
     wn += key[s] < 0x80000000u ? wq : 0u;  // ratio < 0
   }
-  const float rho = Tq > 0.0 ? (float)(P.lam / (Tq * unit)) : 0.f;
   const float d = ws > 0 ? 1.f - 2.f * (float)wn / (float)ws : 1.f;
-  const float f = d < -rho ? 0.5f * (1.f + rho) : (d >= rho ? 0.5f * (1.f - rho) : 0.5f);
-  const float t = f * (float)ws;
-  unsigned c = 0;
-  int sstar = kSample - 1;
-  bool got = false;  // first s with prefix weight > t
+  auto crossing = [&](double lam) {  // first s with prefix weight > the lam-shifted median
+    const float rho = Tq > 0.0 ? (float)(lam / (Tq * unit)) : 0.f;
+    const float f = d < -rho ? 0.5f * (1.f + rho) : (d >= rho ? 0.5f * (1.f - rho) : 0.5f);
+    const float t = f * (float)ws;
+    unsigned c = 0;
+    int ss = kSample - 1;
+    bool got = false;
 #pragma unroll
-  for (int s = 0; s < kSample; ++s) {
-    c += key[s] & 0xffu;
-    if (!got && (float)c > t) { sstar = s; got = true; }
-  }
-  const int lo_i = max(sstar - delta, 0), hi_i = min(sstar + delta, kSample - 1);
+    for (int s = 0; s < kSample; ++s) {
+      c += key[s] & 0xffu;
+      if (!got && (float)c > t) { ss = s; got = true; }
+    }
+    return ss;
+  };
+  const int sstar = crossing(lam_lo);
+  const bool multi = lam_hi > lam_lo;
+  const int s2 = multi ? crossing(lam_hi) : sstar;
+  const int lo_i = max(min(sstar, s2) - delta, 0), hi_i = min(max(sstar, s2) + delta, kSample - 1);
   unsigned kl = 0, kh = 0, kce = 0;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
@@ -283,6 +291,10 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
     const float e = fmaxf(fabsf(l), 1e-30f) * 1e-3f;
     l -= e;
     hh += e;
+  }
+  if (multi && Tq > 0.0 && fabsf(d) <= (float)(lam_hi / (Tq * unit))) {  // may be dead at lam_hi
+    l = fminf(l, 0.f);
+    hh = fmaxf(hh, 0.f);
   }
   *lo = l;
   *hi = hh;
@@ -309,7 +321,7 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 // are also split over blockIdx.z; every CTA adds its histograms into P.GH
 // (exact integer sums, any order), leaves its residual share in P.GE[z] and
 // (z = 0) the ranges in P.GB, and k_bound_epi finishes each problem.
-template <bool CONT, bool SPLIT>
+template <bool CONT, bool SPLIT, bool MULTI = false>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
@@ -349,7 +361,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
         b2 = 0.5f * (r.x + r.y);
       } else {
         sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0], P.delta, &b0,
-                       &b1, &b2, &b3, &b4);
+                       &b1, &b2, &b3, &b4, MULTI ? P.lams[0] : P.lam, MULTI ? P.lams[P.nlam - 1] : P.lam);
       }
     }
     float* d = &sbr[half][0][slot];
@@ -478,6 +490,33 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   __syncthreads();
   const bool h = half != 0;
   const double ect = h ? ec1 + sec[slot] : ec;
+  if (MULTI) {
+    // every penalty in P.lams (ascending): the column bounds summed over the
+    // warp's 32 targets (one pivot), one atomic per warp and penalty
+    const bool okh = h ? ok[1] : ok[0], dgh = h ? degen[1] : degen[0];
+    const bool live = okh && j < m && !dgh && j != (h ? p[1] : p[0]);
+    const double ut = h ? unit[1] : unit[0];
+    const int64_t kh = h ? kk[1] : kk[0];
+    for (int l = 0; l < P.nlam; ++l) {
+      double lb = 0.0, ub = 0.0;
+      if (live) {
+        double2 rg;
+        float2 nx;
+        column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
+                      (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut,
+                      P.lams[l], P.colsum[j], n, sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &rg, &nx);
+      } else if (okh && j < m && dgh) {
+        lb = ub = P.colsum[j];  // fit.py:66-72: v = 0, error = sum |x|
+      }
+      lb = warp_sum(lb);
+      ub = warp_sum(ub);
+      if (lane == 0 && okh) {
+        atomicAdd(&P.LBm[l * P.npiv + kh], lb);
+        atomicAdd(&P.UBm[l * P.npiv + kh], ub);
+      }
+    }
+    return;
+  }
   if (j >= m || !(h ? ok[1] : ok[0])) return;
   const int64_t o = (h ? kk[1] : kk[0]) * m + j;
   if (SPLIT) {
@@ -540,4 +579,14 @@ __global__ void k_bound_epi(SelParams P, int nsplit) {
                 P.lam, P.colsum[j], P.n, g[3], g[4], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
+}
+
+// Penalty of v_p = 1 for every pivot and penalty of a multi-penalty pass.
+__global__ void k_bound_finish(SelParams P, double* __restrict__ lb, double* __restrict__ ub) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.npiv * P.nlam) return;
+  const int64_t l = t / P.npiv, kk = t - l * P.npiv;
+  const double pen = P.nnz[pivot_of(P, kk)] ? P.lams[l] : 0.0;
+  lb[t] += pen;
+  ub[t] += pen;
 }

@@ -85,6 +85,10 @@ struct SelParams {
   unsigned* GH;          // split bound: merged histograms [npiv*m][64]
   double* GE;            // split bound: residual shares [z][npiv*m]
   float* GB;             // split bound: ranges [npiv*m][5]
+  const double* lams;    // multi-penalty bound: ascending penalties (device)
+  int nlam;
+  double* LBm;           // multi-penalty bound: per (penalty, pivot) sums [nlam][npiv]
+  double* UBm;
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {

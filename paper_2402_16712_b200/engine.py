@@ -243,6 +243,21 @@ class DeviceFit:
             bh = b.cpu().numpy()
         return bh[0], bh[1]
 
+    def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
+        """One bounding pass for several strictly ascending penalties: lb, ub [L][npiv] (host)."""
+        lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
+        if npiv is None:
+            npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, lam.size, npiv), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_pivots_multi(
+                self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), lam.size,
+                p_begin, p_stride, npiv, b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                self._s)
+            _lib.check(rc, "l1b_bound_pivots_multi")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
     def bound_pivot_list(self, lam: float, pivots, passes: int = REFINE_PASSES):
         """Bounds for an explicit pivot list; passes 2-3 refine the optimum's range."""
         piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
@@ -336,8 +351,20 @@ class DeviceFit:
             V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
             obj_h = obj.cpu().numpy()
             return [self._winner(float(lam[l]), all_piv, V[l], obj_h[l]) for l in range(lam.size)]
+        # several penalties: one bounding pass for all of them (the histogram
+        # is penalty-free; each penalty gets its own bounds from it)
+        uniq = np.unique(lam[np.isfinite(lam)])
+        multi = None
+        if uniq.size > 1 and all(np.isfinite(lam)):
+            lbm, ubm = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv)
+            multi = {float(x): (lbm[i], ubm[i]) for i, x in enumerate(uniq)}
         for l in range(lam.size):
-            lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
+            if multi is not None:
+                lb, ub = multi[float(lam[l])]
+                fresh = True  # the next level starts from samples at this penalty
+            else:
+                lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
+                fresh = False
             top = float(np.min(ub))
             if ub_exchange is not None:
                 top = float(ub_exchange(top))  # the best upper bound over every shard
@@ -347,13 +374,17 @@ class DeviceFit:
                 out.append(None)
                 continue
             seed, seed_n = keep, npiv  # positions in the last bound call's pivot list
-            for _ in range(REFINE_PASSES):
-                if keep.size <= REFINE_MIN:
+            for level in range(REFINE_PASSES + (1 if fresh else 0)):
+                if keep.size <= REFINE_MIN and not (fresh and level == 0):
                     break
                 # refine the survivors: one more pass each, over the range
                 # where the last pass proved each column's optimum lies, so
-                # the bounds tighten by orders of magnitude per level
-                lb2, ub2 = self.bound_pivot_list_continue(float(lam[l]), all_piv[keep], seed, seed_n)
+                # the bounds tighten by orders of magnitude per level (after
+                # a multi-penalty pass: first one pass at this penalty alone)
+                if fresh and level == 0:
+                    lb2, ub2 = self.bound_pivot_list(float(lam[l]), all_piv[keep], passes=1)
+                else:
+                    lb2, ub2 = self.bound_pivot_list_continue(float(lam[l]), all_piv[keep], seed, seed_n)
                 top = min(top, float(np.min(ub2)))
                 sel = np.nonzero(~(lb2 > self._prune_threshold(top)))[0]
                 keep, seed, seed_n = keep[sel], sel, keep.size

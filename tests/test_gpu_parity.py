@@ -445,3 +445,23 @@ def test_sharded_pruning_with_global_threshold():
         best = min(wins, key=lambda w: (w.objective, w.pivot))
         assert best.pivot == want.pivot and best.v.tobytes() == want.v.tobytes()
         assert best.objective == want.objective
+
+
+def test_multi_penalty_bound_pass():
+    """l1b_bound_pivots_multi: one pass bounds every penalty of a sweep
+    (lb <= z <= ub per penalty and pivot), and the pruned sweep equals the
+    unpruned one."""
+    d, _ = l1b.gen_line_data(70, 1200, seed=4, noise_scale=1.0)
+    X = d.values
+    T = float(np.abs(X).sum(axis=0).max())
+    lams = np.array([0.0, 0.5, 3.0, 0.05 * T, 0.3 * T, 0.9 * T, 1.5 * T])
+    eng = DeviceFit(X)
+    lb, ub = eng.bound_pivots_multi(lams)
+    _, _, _, O = eng.fit_pivots(lams, want_v=False)
+    O = O.cpu().numpy()
+    tol = 1e-12 * np.abs(O) + OBJ_ATOL * float(np.abs(X).sum())
+    assert np.all(lb <= O + tol) and np.all(O <= ub + tol)
+    full = eng.shard_winners(lams, prune=False)
+    pruned = eng.shard_winners(lams[::-1], prune=True)[::-1]  # any order, repeated penalties allowed
+    for a, b in zip(full, pruned):
+        assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes() and a.objective == b.objective
