@@ -84,6 +84,18 @@ int l1b_fit_pivot_list(const double* d_X, int64_t n, int64_t m, const double* h_
 int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
                      int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Algorithm 2 (path.py:76-102) for one pivot: for every target column
+ * c (targets j != pivot in ascending order) the tableau's column in stable
+ * (ratio, row) order (ratios.py:109-135): d_ratios[c*ld + k] = r_k,
+ * d_start[c*ld + k] = sgn(r_k)((T - P_k) - P_{k-1}) - w_k and
+ * d_right[c*ld + k] = start + 2 w_k, k < *h_nrows (the pivot's nonzero
+ * rows), bit-identical to the reference's NumPy arithmetic.  With all three
+ * outputs NULL it only reports *h_nrows (0: zero pivot column, the
+ * reference's EmptyPivotError).  Needs l1b_prepare; *h_nrows <= 16384. */
+int l1b_pivot_breakpoints(const double* d_X, int64_t n, int64_t m, int64_t pivot, int64_t* h_nrows,
+                          double* d_ratios, double* d_start, double* d_right, int64_t ld, void* d_ws,
+                          size_t ws_bytes, void* stream);
+
 /* l1b_bound_pivots for nlam penalties (strictly ascending, host memory) in
  * ONE pass: the histogram range covers the crossings of the smallest and
  * largest penalty (and 0 where the largest may kill the column), and every

@@ -1,0 +1,113 @@
+// path.cuh -- Algorithm 2 (per-pivot breakpoints) on the device (included
+// by l1b200.cu after select.cuh).
+//
+// pivot_breakpoints (path.py:76-102) needs, for one pivot p and every target
+// j != p, the column of the sorted tableau (ratios.py:109-135): the ratios
+// x_ij / x_ip of the rows with x_ip != 0 in stable (ratio, row) order, their
+// weights |x_ip|, the sequential prefix sums P_k (np.cumsum), and
+//   center_k = (T - P_k) - P_{k-1},  start_k = sgn(r_k) center_k - w_k,
+//   right_k  = start_k + 2 w_k        (sgn(r) = +1 iff r >= 0.0).
+// k_breakpoints does one target column per CTA: exact ratios (the hoisted
+// division, bit-identical to IEEE division) keyed by (key64, row), a bitonic
+// sort of the column in shared memory, then the prefix walk in order by one
+// thread (sequential, so the sums round exactly as np.cumsum's do).  The host
+// keeps the live runs (right > 0) and builds the entry tuples.
+
+constexpr int kBpThreads = 1024;
+constexpr int64_t kBpMaxRows = 16384;  // nonzero rows of the pivot a CTA can sort in shared memory
+
+template <bool SAFE>
+__global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t p, int64_t np2, int64_t ld,
+                                                            double* __restrict__ rs, double* __restrict__ st,
+                                                            double* __restrict__ rt) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(psm);
+  int* row = reinterpret_cast<int*>(psm + np2 * sizeof(unsigned long long));
+  __shared__ int cnt_s;
+  const int tid = threadIdx.x;
+  const int64_t n = P.n, m = P.m;
+  const int64_t c = blockIdx.x;           // target column index among j != p
+  const int64_t j = c < p ? c : c + 1;
+  const double* xc = P.Xc + j * n;
+  const double* pb = P.pb + p * P.np;
+  const double* py = P.py + p * P.np;
+  if (tid == 0) cnt_s = 0;
+  __syncthreads();
+  // compact the rows with x_ip != 0 in row order (ratios.py:115): a block-wide
+  // ordered compaction, 1024 rows at a time
+  __shared__ int wsum[kBpThreads / 32];
+  int base = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += kBpThreads) {
+    const int64_t i = i0 + tid;
+    const bool nz = i < n && pb[i] != 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int k = 0; k < kBpThreads / 32; ++k) {
+      off += k < w ? wsum[k] : 0;
+      tot += wsum[k];
+    }
+    if (nz) {
+      const int pos = base + off + __popc(bal & ((1u << l) - 1));
+      key[pos] = key64(sratio<SAFE>(P, xc[i], pb[i], py[i]));
+      row[pos] = (int)i;
+    }
+    base += tot;
+    __syncthreads();
+  }
+  const int cnt = base;
+  for (int64_t e = cnt + tid; e < np2; e += kBpThreads) {
+    key[e] = ~0ULL;
+    row[e] = 0x7fffffff;
+  }
+  __syncthreads();
+  // stable order = ascending (key, row) (np.argsort(kind="stable"), +-0 tied)
+  for (int64_t kq = 2; kq <= np2; kq <<= 1) {
+    for (int64_t jq = kq >> 1; jq > 0; jq >>= 1) {
+      for (int64_t e = tid; e < np2; e += kBpThreads) {
+        const int64_t l = e ^ jq;
+        if (l > e) {
+          const unsigned long long ka = key[e], kb = key[l];
+          const int ra = row[e], rb = row[l];
+          const bool gt = ka > kb || (ka == kb && ra > rb);
+          if (gt == ((e & kq) == 0)) {
+            key[e] = kb;
+            key[l] = ka;
+            row[e] = rb;
+            row[l] = ra;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // the tableau's column totals first (T = P_last, ratios.py:124,134)
+  __shared__ double Tsh;
+  if (tid == 0) {
+    double P = 0.0;
+    for (int k = 0; k < cnt; ++k) P = __dadd_rn(P, fabs(pb[row[k]]));
+    Tsh = P;
+  }
+  __syncthreads();
+  // the per-position runs (path.py:86-89), in sorted order
+  if (tid == 0) {
+    const double T = Tsh;
+    double Pp = 0.0;  // prefix_prev
+    for (int k = 0; k < cnt; ++k) {
+      const int r = row[k];
+      const double w = fabs(pb[r]);
+      const double Pk = __dadd_rn(Pp, w);
+      double ratio = sratio<SAFE>(P, xc[r], pb[r], py[r]);
+      if (ratio == 0.0) ratio = __ddiv_rn(xc[r], pb[r]);  // the zero's sign (the hoisted path may drop it)
+      const double center = __dsub_rn(__dsub_rn(T, Pk), Pp);
+      const double s = __dsub_rn(ratio >= 0.0 ? center : -center, w);
+      const double rr = __dadd_rn(s, __dmul_rn(2.0, w));
+      rs[c * ld + k] = ratio;
+      st[c * ld + k] = s;
+      rt[c * ld + k] = rr;
+      Pp = Pk;
+    }
+  }
+}

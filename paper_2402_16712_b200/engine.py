@@ -243,6 +243,26 @@ class DeviceFit:
             bh = b.cpu().numpy()
         return bh[0], bh[1]
 
+    def pivot_runs(self, pivot: int):
+        """Sorted tableau runs of one pivot (l1b_pivot_breakpoints): ratios, starts and
+        right ends [m-1][n_p] in sorted order per target column, or (None, None, None)
+        for a zero pivot column."""
+        nr = ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_pivot_breakpoints(self.X.data_ptr(), self.n, self.m, int(pivot),
+                                                      ctypes.byref(nr), None, None, None, 0, self.ws.data_ptr(),
+                                                      self.ws.numel(), self._s), "l1b_pivot_breakpoints")
+            k = int(nr.value)
+            if k == 0:
+                return None, None, None
+            out = torch.empty((3, self.m - 1, k), dtype=torch.float64, device=self.device)
+            _lib.check(self.lib.l1b_pivot_breakpoints(self.X.data_ptr(), self.n, self.m, int(pivot),
+                                                      ctypes.byref(nr), out[0].data_ptr(), out[1].data_ptr(),
+                                                      out[2].data_ptr(), k, self.ws.data_ptr(), self.ws.numel(),
+                                                      self._s), "l1b_pivot_breakpoints")
+            h = out.cpu().numpy()
+        return h[0], h[1], h[2]
+
     def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
         """One bounding pass for several strictly ascending penalties: lb, ub [L][npiv] (host)."""
         lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))

@@ -1,0 +1,156 @@
+"""Algorithm 2 on the B200: per-pivot breakpoints of the regularisation path.
+
+Mirror of the reference's ``l1line.path`` front half ("next"
+row 1), same names, fields and semantics:
+
+* ``PivotBreakpoints`` / ``pivot_breakpoints(data, pivot)``  <- path.py:38-102
+* ``PivotSolutions`` / ``major_breakpoints(data, threads)``   <- path.py:105-154
+
+For every column of a pivot, sorted position k of the tableau holds the
+optimum for the half-open run of penalties starting at
+``start_k = sgn(r_k) (T - P_k - P_{k-1}) - w_k`` of width ``2 w_k``; runs whose
+right end is not positive are dropped, starts clamp at 0, and the largest
+right end is the column's death weight.  The device
+(``l1b_pivot_breakpoints``, ``csrc/path.cuh``) computes the exact ratios,
+the stable sort of every column and the sequential prefix sums -- the
+reference's 84 % -- bit for bit; this module keeps the
+live runs and builds the same entry tuples.  The envelope merge
+(Algorithm 3, ``merge_path``) is not ported.
+"""
+
+from __future__ import annotations
+
+from bisect import bisect_right
+from dataclasses import dataclass
+
+import numpy as np
+
+from .api import _as_data, resolve_threads
+from .core import DataMatrix, EmptyPivotError
+from .engine import DeviceFit
+
+__all__ = ["PivotBreakpoints", "PivotSolutions", "pivot_breakpoints", "major_breakpoints", "DEDUP_TOL"]
+
+DEDUP_TOL = 1e-9  # path.py:34: breakpoints closer than this (absolute) are one
+
+
+@dataclass(frozen=True)
+class PivotBreakpoints:
+    """Piecewise-constant snap values of every column of one pivot (path.py:38-73).
+
+    ``entries[target]``: ascending (weight, value) pairs, the column takes
+    ``value`` from that weight on; the last pair is (lambda_max[target], 0.0).
+    """
+
+    pivot: int
+    entries: dict[int, tuple[tuple[float, float], ...]]
+    lambda_max: dict[int, float]
+
+    def column_value(self, target: int, lam: float) -> float:
+        if lam < 0.0:
+            raise ValueError("penalty weight must be nonnegative")
+        entries = self.entries[target]
+        return entries[bisect_right([bp for bp, _ in entries], lam) - 1][1]
+
+    def breakpoint_set(self) -> set[float]:
+        out: set[float] = set()
+        for target, entries in self.entries.items():
+            out.add(self.lambda_max[target])
+            out.update(bp for bp, _ in entries[:-1] if bp > 0.0)
+        return out
+
+
+def _maps(pivot: int, m: int, rs: np.ndarray, st: np.ndarray, rt: np.ndarray,
+          weights: list | None = None) -> PivotBreakpoints:
+    entries: dict[int, tuple[tuple[float, float], ...]] = {}
+    lambda_max: dict[int, float] = {}
+    targets = [j for j in range(m) if j != pivot]
+    for c, target in enumerate(targets):
+        right = rt[c]
+        live = right > 0.0
+        # (max(0, start), r) for the live runs in sorted order, then (death, 0.0),
+        # stably ordered by weight (path.py:92-97); max(0.0, x) == (x if x > 0.0 else 0.0)
+        s_live = st[c][live]
+        w = np.append(np.where(s_live > 0.0, s_live, 0.0), max(0.0, float(right.max())))
+        val = np.append(rs[c][live], 0.0)
+        order = np.argsort(w, kind="stable")
+        entries[target] = tuple(zip(w[order].tolist(), val[order].tolist()))
+        lambda_max[target] = float(w[-1])
+        if weights is not None:
+            weights.append(w)
+    return PivotBreakpoints(pivot=pivot, entries=entries, lambda_max=lambda_max)
+
+
+def _pivot_maps(eng: DeviceFit, pivot: int, weights: list | None = None) -> PivotBreakpoints:
+    rs, st, rt = eng.pivot_runs(pivot)
+    if rs is None:
+        raise EmptyPivotError(f"column {pivot} is identically zero")
+    return _maps(pivot, eng.m, rs, st, rt, weights)
+
+
+def _dedup(vals: np.ndarray) -> np.ndarray:
+    """path.py:146-152 on an array: keep v when v - (last kept) > DEDUP_TOL, ascending.
+
+    Exact duplicates never survive, so np.unique first changes nothing; an
+    element more than DEDUP_TOL above its predecessor is always kept (the last
+    kept value is at most the predecessor), so only runs of closer neighbours
+    need the sequential rule."""
+    u = np.unique(vals)
+    keep = np.ones(u.size, dtype=bool)
+    close = np.nonzero(np.diff(u) <= DEDUP_TOL)[0] + 1
+    if close.size:
+        starts = close[np.concatenate(([True], np.diff(close) > 1))]
+        ends = close[np.concatenate((np.diff(close) > 1, [True]))]
+        for a, b in zip(starts.tolist(), ends.tolist()):
+            last = float(u[a - 1])
+            for i in range(a, b + 1):
+                x = float(u[i])
+                if x - last > DEDUP_TOL:
+                    last = x
+                else:
+                    keep[i] = False
+    return u[keep]
+
+
+def pivot_breakpoints(data, pivot: int) -> PivotBreakpoints:
+    """Closed-form breakpoints of one pivot's snap values (path.py:76-102)."""
+    d = _as_data(data)
+    if not 0 <= pivot < d.m:
+        raise IndexError(f"pivot column {pivot} out of range")
+    return _pivot_maps(DeviceFit(d.values, max_pivots=1), int(pivot))
+
+
+@dataclass(frozen=True)
+class PivotSolutions:
+    """Breakpoint maps of every usable pivot plus the degenerate ones (path.py:105-125)."""
+
+    data: DataMatrix
+    pivots: dict[int, PivotBreakpoints]
+    degenerate: tuple[int, ...]
+
+    def solution_at(self, pivot: int, lam: float) -> np.ndarray:
+        v = np.zeros(self.data.m)
+        if pivot in self.pivots:
+            v[pivot] = 1.0
+            for target, entries in self.pivots[pivot].entries.items():
+                v[target] = entries[bisect_right([bp for bp, _ in entries], lam) - 1][1]
+        elif pivot not in self.degenerate:
+            raise IndexError(f"unknown pivot {pivot}")
+        return v
+
+
+def major_breakpoints(data, threads: int | None = None) -> tuple[np.ndarray, PivotSolutions]:
+    """Every weight where some pivot's own solution changes (path.py:127-154):
+    the ascending deduplicated grid (starting at 0) and the per-pivot maps."""
+    resolve_threads(threads)
+    d = _as_data(data)
+    eng = DeviceFit(d.values, max_pivots=1)  # K0 once; one device pass per pivot
+    pivots: dict[int, PivotBreakpoints] = {}
+    degenerate = []
+    weights = [np.zeros(1)]  # the grid always starts at 0
+    for p in range(d.m):
+        try:
+            pivots[p] = _pivot_maps(eng, p, weights)
+        except EmptyPivotError:
+            degenerate.append(p)
+    return _dedup(np.concatenate(weights)), PivotSolutions(d, pivots, tuple(degenerate))

@@ -163,11 +163,56 @@ def datagen_cases():
     np.savez_compressed(os.path.join(OUT, "datagen.npz"), **out)
 
 
+def _flat_breakpoints(pb):
+    """pivot_breakpoints (path.py:76-102) as arrays: rows (target, weight, value) in
+    the dict's target order, each target's entries in tuple order; lambda_max per target."""
+    rows, lmax = [], []
+    for target, entries in pb.entries.items():
+        for bp, val in entries:
+            rows.append((float(target), bp, val))
+        lmax.append((float(target), pb.lambda_max[target]))
+    return np.asarray(rows, dtype=np.float64).reshape(-1, 3), np.asarray(lmax, dtype=np.float64).reshape(-1, 2)
+
+
+def breakpoint_cases():
+    """Algorithm 2 (path.py:76-154): per-pivot breakpoint maps and the merged grid."""
+    toy = np.array([[4.0, -2.0, 3.0, -6.0], [-3.0, 4.0, 2.0, -1.0], [2.0, 3.0, -3.0, -2.0],
+                    [-3.0, 4.0, 2.0, 3.0], [5.0, 3.0, 2.0, -1.0]])
+    rng = np.random.default_rng(77)
+    cases = [("toy", toy)]
+    for t in range(12):
+        n, m = int(rng.integers(1, 40)), int(rng.integers(2, 8))
+        X = rng.uniform(-10, 10, size=(n, m))
+        if t % 4 == 1:
+            X[rng.random(X.shape) < 0.3] = 0.0
+        elif t % 4 == 2:
+            X = np.round(X)
+            X[rng.random(X.shape) < 0.2] = -0.0
+        elif t % 4 == 3:
+            X[:, int(rng.integers(m))] = 0.0
+        cases.append((f"rand{t}", X))
+    cases.append(("line", l1line.gen_line_data(12, 300, seed=5, noise_scale=1.0)[0].values))
+    cases.append(("tall", np.round(l1line.gen_line_data(6, 3000, seed=9, noise_scale=0.5)[0].values * 2**10) / 2**10))
+    out = {"names": np.asarray([c[0] for c in cases])}
+    for name, X in cases:
+        d = l1line.DataMatrix(X)
+        out[f"{name}_X"] = X
+        lambdas, sols = l1line.major_breakpoints(d, threads=1)
+        out[f"{name}_grid"] = lambdas
+        out[f"{name}_degenerate"] = np.asarray(sols.degenerate, dtype=np.int64)
+        for p in range(X.shape[1]):
+            if p in sols.pivots:
+                rows, lmax = _flat_breakpoints(sols.pivots[p])
+                out[f"{name}_p{p}_entries"] = rows
+                out[f"{name}_p{p}_lmax"] = lmax
+    np.savez_compressed(os.path.join(OUT, "breakpoints.npz"), **out)
+
+
 if __name__ == "__main__":
-    random_small()
-    c1_and_grid()
-    subspace_cases()
-    datagen_cases()
+    want = set(sys.argv[1:])
+    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases):
+        if not want or f.__name__ in want:
+            f()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -465,3 +465,58 @@ def test_multi_penalty_bound_pass():
     pruned = eng.shard_winners(lams[::-1], prune=True)[::-1]  # any order, repeated penalties allowed
     for a, b in zip(full, pruned):
         assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes() and a.objective == b.objective
+
+
+# ------------------------------------------- Algorithm 2 (path.py, "next") --
+
+THIRD = 1.0 / 3.0
+
+
+def test_pivot_breakpoints_toy_known_answers():
+    """pkg/tests/test_path.py:33-70 (toy entry maps, death weights, breakpoint sets)."""
+    from paper_2402_16712_b200 import pivot_breakpoints
+    expected = {
+        0: {1: ((0.0, -0.5), (3.0, 0.0)), 2: ((0.0, 0.4), (1.0, 0.0)),
+            3: ((0.0, -1.0), (1.0, -0.2), (11.0, 0.0))},
+        1: {0: ((0.0, -0.75), (4.0, 0.0)), 2: ((0.0, 0.5), (6.0, 0.0)), 3: ((0.0, -0.25), (4.0, 0.0))},
+        2: {0: ((0.0, -2.0 * THIRD), (2.0, 0.0)), 1: ((0.0, 0.0),), 3: ((0.0, -0.5), (2.0, 0.0))},
+        3: {0: ((0.0, -2.0 * THIRD), (11.0, 0.0)), 1: ((0.0, THIRD), (5.0, 0.0)), 2: ((0.0, -0.5), (3.0, 0.0))},
+    }
+    for pivot, entries in expected.items():
+        pb = pivot_breakpoints(TOY, pivot)
+        assert pb.pivot == pivot and pb.entries == entries
+    assert pivot_breakpoints(TOY, 0).lambda_max == {1: 3.0, 2: 1.0, 3: 11.0}
+    sets = [pivot_breakpoints(TOY, p).breakpoint_set() for p in range(4)]
+    assert sets == [{1.0, 3.0, 11.0}, {4.0, 6.0}, {0.0, 2.0}, {3.0, 5.0, 11.0}]
+    pb = pivot_breakpoints(TOY, 0)
+    assert [pb.column_value(3, x) for x in (0.0, 0.999, 1.0, 11.0, 1e6)] == [-1.0, -1.0, -0.2, 0.0, 0.0]
+    with pytest.raises(ValueError):
+        pb.column_value(3, -0.5)
+    with pytest.raises(IndexError):
+        pivot_breakpoints(TOY, 4)
+
+
+def test_major_breakpoints_match_reference_fixtures():
+    """Every pivot's entry map, death weights and the merged grid equal the
+    reference's (tests/golden/breakpoints.npz, from l1line.major_breakpoints),
+    bit for bit: toy, ragged random instances with zeros / -0.0 / ties / zero
+    columns, a 300x12 line and a 3000x6 grid-quantised tall case."""
+    from paper_2402_16712_b200 import major_breakpoints
+    from paper_2402_16712_b200.path import EmptyPivotError, pivot_breakpoints
+    g = load_golden("breakpoints.npz")
+    for name in g["names"]:
+        X = g[f"{name}_X"]
+        grid, sols = major_breakpoints(X)
+        assert grid.tobytes() == g[f"{name}_grid"].tobytes(), name
+        assert sols.degenerate == tuple(int(p) for p in g[f"{name}_degenerate"]), name
+        for p in range(X.shape[1]):
+            if p in sols.degenerate:
+                with pytest.raises(EmptyPivotError):
+                    pivot_breakpoints(X, p)
+                continue
+            pb = sols.pivots[p]
+            rows = np.asarray([(t, bp, v) for t, e in pb.entries.items() for bp, v in e], dtype=np.float64)
+            lmax = np.asarray([(t, pb.lambda_max[t]) for t in pb.entries], dtype=np.float64)
+            assert rows.tobytes() == g[f"{name}_p{p}_entries"].tobytes(), (name, p)
+            assert lmax.tobytes() == g[f"{name}_p{p}_lmax"].tobytes(), (name, p)
+        assert sols.solution_at(int(np.argmax([p in sols.pivots for p in range(X.shape[1])])), 0.0).shape == (X.shape[1],)

@@ -157,3 +157,18 @@ def test_abi_sass_is_sm100a():
     so = _lib.LIB_PATH
     out = subprocess.run(["cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_breakpoint_grid_dedup_matches_reference_rule():
+    """path.major_breakpoints' vectorised dedup == path.py:146-152's sequential rule."""
+    from paper_2402_16712_b200.path import DEDUP_TOL, _dedup
+    rng = np.random.default_rng(0)
+    for t in range(100):
+        v = np.concatenate([rng.uniform(0, 1e-7, 40), np.round(rng.uniform(0, 5, 80), 2),
+                            rng.uniform(0, 1e-8, 20) + 3.0, np.zeros(5), rng.uniform(0, 1e-9, 10) + 1.0])
+        vals = sorted([0.0] + v.tolist())
+        ref = [vals[0]]
+        for x in vals[1:]:
+            if x - ref[-1] > DEDUP_TOL:
+                ref.append(x)
+        assert np.asarray(ref).tobytes() == _dedup(np.concatenate([[0.0], v])).tobytes(), t
