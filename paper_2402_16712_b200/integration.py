@@ -18,7 +18,8 @@ _PATCHED = {}
 
 
 def use_gpu(module: str = "l1line") -> None:
-    """Patch ``l1line`` in place so fit_line / fit_for_pivot / fit_subspace use the GPU."""
+    """Patch ``l1line`` in place so fit_line / fit_for_pivot / fit_subspace and the
+    breakpoint maps (pivot_breakpoints / major_breakpoints, so solution_path too) use the GPU."""
     from . import api
 
     l1 = importlib.import_module(module)
@@ -40,12 +41,32 @@ def use_gpu(module: str = "l1line") -> None:
         fit = api.fit_subspace(data, lam, k, threads)
         return sub.SubspaceFit(tuple(_conv(c) for c in fit.components), fit.degenerate)
 
+    def _ref_path():
+        return importlib.import_module(f"{module}.path")
+
+    def pivot_breakpoints(data, pivot):
+        from . import path
+        pb = path.pivot_breakpoints(data, pivot)
+        return _ref_path().PivotBreakpoints(pivot=pb.pivot, entries=pb.entries, lambda_max=pb.lambda_max)
+
+    def major_breakpoints(data, threads=None):
+        # Algorithm 2 on the device; the reference's merge_path / solution_path
+        # (Algorithm 3) then run unchanged on the result
+        from . import path
+        rp = _ref_path()
+        grid, sols = path.major_breakpoints(data, threads)
+        pivots = {p: rp.PivotBreakpoints(pivot=pb.pivot, entries=pb.entries, lambda_max=pb.lambda_max)
+                  for p, pb in sols.pivots.items()}
+        return grid, rp.PivotSolutions(data, pivots, sols.degenerate)
+
     targets = {
         "fit_line": fit_line,
         "fit_for_pivot": fit_for_pivot,
         "fit_subspace": fit_subspace,
+        "pivot_breakpoints": pivot_breakpoints,
+        "major_breakpoints": major_breakpoints,
     }
-    for modname in ("", ".fit", ".subspace", ".oracle", ".cli"):
+    for modname in ("", ".fit", ".subspace", ".oracle", ".cli", ".path"):
         try:
             mod = importlib.import_module(module + modname)
         except ImportError:

@@ -315,15 +315,23 @@ def test_use_gpu_patches_reference_bindings():
     sub = types.ModuleType("fake_l1line.subspace")
     sub.fit_line = None
     sub.SubspaceFit = l1b.SubspaceFit
-    sys.modules.update({"fake_l1line": pkg, "fake_l1line.core": core, "fake_l1line.subspace": sub})
+    from paper_2402_16712_b200 import path as our_path
+    pth = types.ModuleType("fake_l1line.path")
+    pth.major_breakpoints = None
+    pth.PivotBreakpoints = our_path.PivotBreakpoints
+    pth.PivotSolutions = our_path.PivotSolutions
+    sys.modules.update({"fake_l1line": pkg, "fake_l1line.core": core, "fake_l1line.subspace": sub,
+                        "fake_l1line.path": pth})
     try:
         from paper_2402_16712_b200.integration import restore, use_gpu
         use_gpu("fake_l1line")
         assert pkg.fit_line(TOY, 0.0).preserved == 3 and sub.fit_line(TOY, 5.0).preserved == 0
+        grid, sols = pth.major_breakpoints(l1b.DataMatrix(TOY))  # what solution_path calls (path.py:280-282)
+        assert grid.tolist() == [0.0, 1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 11.0] and sorted(sols.pivots) == [0, 1, 2, 3]
         restore()
-        assert pkg.fit_line is None
+        assert pkg.fit_line is None and pth.major_breakpoints is None
     finally:
-        for k in ("fake_l1line", "fake_l1line.core", "fake_l1line.subspace"):
+        for k in ("fake_l1line", "fake_l1line.core", "fake_l1line.subspace", "fake_l1line.path"):
             sys.modules.pop(k, None)
 
 
