@@ -399,6 +399,15 @@ def run_ours(args):
                                         "8 in flight per thread)",
                          "fp32_view": {"ops_per_element": 5, "achieved_TOPs": 5 * kb_rate / 1e12,
                                        "peak_TOPs": _fp32_peak(dev) / 1e12},
+                         "smem_wavefront_view": {
+                             "note": "shared-memory pipe cycles the design needs per element: per warp, 4 rows x "
+                                     "2 pivots x 32 targets cost 4 tile + 6 plane loads + 8 atomics = 18 "
+                                     "wavefronts; peak = one wavefront per SM-clock (the atomic probe / 32). "
+                                     "ncu (profiles/r01/ncu_bound_c2_v13.txt) measures the L1/TEX pipe at 78 %.",
+                             "wavefronts_per_element": 18.0 / 256.0,
+                             "achieved_G_per_s": kb_rate * 18.0 / 256.0 / 1e9,
+                             "peak_G_per_s": atoms_peak / 32.0 / 1e9,
+                             "frac": kb_rate * 18.0 / 256.0 / (atoms_peak / 32.0)},
                          "step_view": {
                              "note": "whole pruned step against the exact algorithm's FP64 floor (SURVEY.md 8d: "
                                      "11 FP64 ops per ratio element, E = n*m*(m-1) per fit); > 1 means the step "
