@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -83,7 +84,9 @@ def _upload(Xh: np.ndarray, device: torch.device) -> torch.Tensor:
             _STAGING[key] = [(torch.empty(_STAGE_DOUBLES, dtype=torch.float64).pin_memory(), torch.cuda.Event())
                              for _ in range(2)]
     stage = _STAGING[key]
-    src = torch.from_numpy(Xh.reshape(-1))
+    with warnings.catch_warnings():  # read-only inputs (DataMatrix.values) are only read here
+        warnings.simplefilter("ignore", UserWarning)
+        src = torch.from_numpy(Xh.reshape(-1))
     with torch.cuda.device(device):
         dst = torch.empty(Xh.shape, dtype=torch.float64, device=device)
         flat = dst.view(-1)
@@ -112,7 +115,12 @@ class DeviceFit:
             Xd = X.to(device=self.device, dtype=torch.float64).contiguous()
         else:
             Xh = np.ascontiguousarray(X, dtype=np.float64)
-            Xd = _upload(Xh, self.device) if Xh.size >= (1 << 16) else torch.from_numpy(Xh).to(self.device)
+            if Xh.size >= (1 << 16):
+                Xd = _upload(Xh, self.device)
+            else:
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore", UserWarning)
+                    Xd = torch.from_numpy(Xh).to(self.device)
         if Xd.dim() != 2:
             raise ValueError(f"expected a 2-d array, got shape {tuple(Xd.shape)}")
         self.X = Xd
