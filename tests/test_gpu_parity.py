@@ -401,7 +401,7 @@ def test_pruned_fit_equals_full_fit():
         d, _ = l1b.gen_line_data(m, n, seed=seed, noise_scale=1.0)
         X = d.values
         T = float(np.abs(X).sum(axis=0).max())
-        lams = [0.0, 1.0, 0.1 * T, 0.5 * T]
+        lams = [0.0, 1.0, 0.1 * T, 0.5 * T, 2.0 * T, math.inf]
         eng = DeviceFit(X)
         full = eng.shard_winners(lams, prune=False)
         pruned = eng.shard_winners(lams, prune=True)  # forced: these sizes are below the auto threshold
