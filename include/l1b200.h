@@ -96,6 +96,14 @@ int l1b_pivot_breakpoints(const double* d_X, int64_t n, int64_t m, int64_t pivot
                           double* d_ratios, double* d_start, double* d_right, int64_t ld, void* d_ws,
                           size_t ws_bytes, void* stream);
 
+/* Optimality certificate of every column of one line (oracle.py:141-174's
+ * dual conditions, checked through the subdifferential with exact weight
+ * sums): d_slack[j] >= 0 iff v_j (device d_v[m]) minimises pivot `pivot`'s
+ * column-j objective at lam; +inf for j == pivot and for a zero pivot column.
+ * In weight units (compare with a tolerance for raw, non-grid inputs). */
+int l1b_certify_columns(const double* d_X, int64_t n, int64_t m, int64_t pivot, const double* d_v, double lam,
+                        double* d_slack, void* d_ws, size_t ws_bytes, void* stream);
+
 /* l1b_bound_pivots for nlam penalties (strictly ascending, host memory) in
  * ONE pass: the histogram range covers the crossings of the smallest and
  * largest penalty (and 0 where the largest may kill the column), and every

@@ -16,9 +16,10 @@ __version__ = "0.1.0"
 _API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
         "residual_error", "resolve_threads")
 _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions")
+_CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
 
 __all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "SubspaceFit", "gen_line_data",
-           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, "__version__"]
+           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, "__version__"]
 
 
 def __getattr__(name):
@@ -29,6 +30,9 @@ def __getattr__(name):
     if name in _PATH:
         from . import path
         return getattr(path, name)
+    if name in _CERT:
+        from . import certify
+        return getattr(certify, name)
     if name == "use_gpu":
         from .integration import use_gpu
         return use_gpu

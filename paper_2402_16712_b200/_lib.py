@@ -39,6 +39,7 @@ ABI_SYMBOLS = (
     "l1b_bound_pivot_list_continue",
     "l1b_bound_pivots_multi",
     "l1b_pivot_breakpoints",
+    "l1b_certify_columns",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -124,6 +125,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_pivot_breakpoints.restype = ctypes.c_int
     lib.l1b_pivot_breakpoints.argtypes = [_vp, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int64), _vp, _vp, _vp, _i64,
                                           _vp, _sz, _vp]
+    lib.l1b_certify_columns.restype = ctypes.c_int
+    lib.l1b_certify_columns.argtypes = [_vp, _i64, _i64, _i64, _vp, ctypes.c_double, _vp, _vp, _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

@@ -111,3 +111,52 @@ __global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t
     }
   }
 }
+
+// ------------------------------------------- optimality certificates --
+//
+// The dual certificate of oracle.py:141-174 for every column of one line at
+// once: v_j minimises f_j(t) = sum_i w_i |r_i - t| + lam |t| iff 0 lies in
+// the subdifferential, i.e. with exact weight sums below / above / at v_j
+// (fixed-point weights wq, exact in any order) and L = lam 2^s_p:
+//   v > 0: |D + L| <= A,  v < 0: |D - L| <= A,  v = 0: |D| <= A + L,
+// D = W(r < v) - W(r > v), A = W(r = v).  The slack (A - |...|, or
+// A + L - |D|) in weight units is >= 0 exactly when a feasible,
+// complementary multiplier vector exists (the reference builds it).  Warp
+// per target column; exact ratios compared through their 64-bit keys.
+template <bool SAFE>
+__global__ void k_certify(SelParams P, int64_t p, const double* __restrict__ v, double lam,
+                          double* __restrict__ slack) {
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int64_t n = P.n, m = P.m, j = warp;
+  if (j >= m) return;
+  if (j == p || P.nnz[p] == 0) {
+    if (lane == 0) slack[j] = INFINITY;
+    return;
+  }
+  const double* xc = P.Xc + j * n;
+  const double* pb = P.pb + p * P.np;
+  const double* py = P.py + p * P.np;
+  const double* pw = P.pw + p * P.np;
+  const double vj = v[j];
+  const unsigned long long kv = key64(vj);
+  double below = 0.0, above = 0.0, at = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    const double w = pw[i];
+    if (w == 0.0) continue;  // x_ip = 0: not in the column (ratios.py:115)
+    const unsigned long long k = key64(sratio<SAFE>(P, xc[i], pb[i], py[i]));
+    below += k < kv ? w : 0.0;
+    above += k > kv ? w : 0.0;
+    at += k == kv ? w : 0.0;
+  }
+  below = warp_sum(below);
+  above = warp_sum(above);
+  at = warp_sum(at);
+  if (lane == 0) {
+    const double L = ldexp(lam, P.spow[p]), D = below - above;
+    double s;
+    if (kv == kZeroKey) s = at + L - fabs(D);
+    else if (vj > 0.0) s = at - fabs(D + L);
+    else s = at - fabs(D - L);
+    slack[j] = ldexp(s, -P.spow[p]);
+  }
+}

@@ -528,3 +528,46 @@ def test_major_breakpoints_match_reference_fixtures():
             assert rows.tobytes() == g[f"{name}_p{p}_entries"].tobytes(), (name, p)
             assert lmax.tobytes() == g[f"{name}_p{p}_lmax"].tobytes(), (name, p)
         assert sols.solution_at(int(np.argmax([p in sols.pivots for p in range(X.shape[1])])), 0.0).shape == (X.shape[1],)
+
+
+# ------------------------------- optimality certificates (oracle.py, "next") --
+
+def test_certificates_toy_and_refutations():
+    """oracle.py:141-174 behaviour (pkg/tests/test_oracle.py:55-110): every
+    solved toy column is certified; wrong values are refuted."""
+    import types
+
+    from paper_2402_16712_b200 import OptimalityRefuted, certify_line, check_line
+    for lam in (0.0, 0.5, 2.0, 3.0, 7.0, 11.0, 15.0):
+        for pivot in range(4):
+            line = l1b.fit_for_pivot(TOY, pivot, lam)
+            cert = check_line(TOY, line)
+            assert cert.ok and np.isinf(cert.slack[pivot])
+    base = l1b.fit_for_pivot(TOY, 0, 0.0)
+    for j, val, lam in ((3, -1.5, 0.0), (3, -0.987, 0.0)):
+        v = base.v.copy()
+        v[j] = val
+        bad = types.SimpleNamespace(v=v, preserved=0, lam=lam)
+        assert certify_line(TOY, bad).refuted == (j,)
+        with pytest.raises(OptimalityRefuted):
+            check_line(TOY, bad)
+    # column (0, 2): 0.4 until it dies at lam 1; at lam 5 only 0.0 is optimal
+    v = l1b.fit_for_pivot(TOY, 0, 5.0).v.copy()
+    assert v[2] == 0.0 and certify_line(TOY, types.SimpleNamespace(v=v, preserved=0, lam=5.0)).ok
+    v[2] = 0.4
+    assert 2 in certify_line(TOY, types.SimpleNamespace(v=v, preserved=0, lam=5.0)).refuted
+
+
+def test_certificates_random_and_at_scale():
+    """Random instances (test_oracle.py:94-110) and a 3000x400 winner: every column certified."""
+    from paper_2402_16712_b200 import check_line
+    from conftest import random_instance
+    rng = np.random.default_rng(8)
+    for _ in range(25):
+        X = random_instance(rng, zeros=True)
+        lam = float(rng.uniform(0.0, 0.7 * np.abs(X).sum()))
+        check_line(X, l1b.fit_line(X, lam))
+    d, _ = l1b.gen_line_data(400, 3000, seed=2, noise_scale=1.0)
+    for lam in (1.0, 500.0):
+        cert = check_line(d, l1b.fit_line(d, lam))
+        assert cert.ok and np.isfinite(cert.slack).sum() == 399
