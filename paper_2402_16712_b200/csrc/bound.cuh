@@ -51,7 +51,10 @@ constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [problem][bin][slot], exact 32
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 // bracket half-width in sample ranks: narrow for the one-pass bound (tight
 // bins), wider when later passes refine it (fewer optima outside)
-constexpr int kBDelta1 = 7, kBDeltaN = 10;
+#ifndef KB_DELTA1
+#define KB_DELTA1 8
+#endif
+constexpr int kBDelta1 = KB_DELTA1, kBDeltaN = 10;
 
 // Bounds of one column optimum from its histogram h[slot * hs] (exact sums
 // of 32-bit weights of q each) over the bracket [lo, hi) (62 interior bins),
