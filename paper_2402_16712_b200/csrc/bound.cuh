@@ -59,7 +59,32 @@ constexpr int kBDelta1 = KB_DELTA1, kBDeltaN = 10;
 // Bounds of one column optimum from its histogram h[slot * hs] (exact sums
 // of 32-bit weights of q each) over the bracket [lo, hi) (62 interior bins),
 // e_j(c) = ec, the exact pivot weight T and the column's sum_i |x_ij| (f(0)).
-__device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double q, double lo, double hi, double c,
+// The histogram column as inclusive prefix sums Cu_k, in place, and the
+// checkpoints SC_{8i} of SC_k = sum_{q<k} Cu_q (exact integers).
+struct Prefix {
+  unsigned* h;
+  int hs;
+  unsigned long long sc8[8];
+  __device__ __forceinline__ void build() {
+    unsigned cu = 0;
+    unsigned long long sc = 0;
+#pragma unroll
+    for (int k = 0; k < kNB; ++k) {
+      if ((k & 7) == 0) sc8[k >> 3] = sc;
+      cu += h[k * hs];
+      h[k * hs] = cu;
+      sc += cu;
+    }
+  }
+  __device__ __forceinline__ unsigned cu(int k) const { return h[k * hs]; }
+  __device__ __forceinline__ unsigned long long sc(int k) const {
+    unsigned long long s = sc8[k >> 3];
+    for (int q = k & ~7; q < k; ++q) s += h[q * hs];
+    return s;
+  }
+};
+
+__device__ __forceinline__ void column_bounds(const Prefix& H, double q, double lo, double hi, double c,
                                               double ec, double T, double lam, double colsum, int64_t n,
                                               float smin, float smax, double* lbo, double* ubo, double2* range,
                                               float2* next) {
@@ -103,31 +128,43 @@ __device__ __forceinline__ void column_bounds(const unsigned* h, int hs, double 
   };
   const long long tLm = thr_le(T - 2.0 * dC + lam), tLp = thr_le(T - 2.0 * dC - lam);  // sm = -1 / +1
   const long long tRm = thr_ge(T + 2.0 * dC + lam), tRp = thr_ge(T + 2.0 * dC - lam);  // sp = -1 / +1
-  int kL = -1, kR = kNB - 1;
-  long long CuL = 0, SCL = 0, CuR = 0, SCR = 0, CuC = 0, SCC = 0, CuC1 = 0, Cu0 = 0, Cu62 = 0, SC62 = 0;
+  // kL = last edge with ghi <= 0, kR = first with glo >= 0: Cu_k grows and
+  // the thresholds only drop at the sign change, so both tests are monotone
+  // in k and two binary searches over the prefix sums find them
+  const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
+  const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
+  const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
+  const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
+  auto pL = [&](int k) {
+    const unsigned cu = H.cu(k);
+    return k >= z1 ? (hasL_p & (cu <= uLp)) : (hasL_m & (cu <= uLm));
+  };
+  auto pR = [&](int k) {
+    const unsigned cu = H.cu(k);
+    return k >= z0 ? (hasR_p & (cu >= uRp)) : (hasR_m & (cu >= uRm));
+  };
+  int kL, kR;
   {
-    // Cu_k < 2^31 (the weights sum to Tq / 2^21 + n / 2): 32-bit compares
-    const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
-    const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
-    const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
-    const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
-    unsigned Cu = 0;
-    long long SC = 0;
-    Cu0 = h[0];
-    for (int k = 0; k <= kNI; ++k) {
-      Cu += h[k * hs];  // Cu_k; SC = SC_k
-      const bool pl = k >= z1, pr = k >= z0;
-      if (pl ? (hasL_p & (Cu <= uLp)) : (hasL_m & (Cu <= uLm))) { kL = k; CuL = Cu; SCL = SC; }
-      const bool r = pr ? (hasR_p & (Cu >= uRp)) : (hasR_m & (Cu >= uRm));
-      if (r & (kR == kNB - 1)) { kR = k; CuR = Cu; SCR = SC; }
-      if (k == kc) { CuC = Cu; SCC = SC; }
-      if (k == kc + 1) CuC1 = Cu;
-      Cu62 = Cu;
-      SC62 = SC;
-      if ((kR < kNB - 1) & (k > kc)) break;  // everything needed is captured
-      SC += Cu;
+    int a = -1, b = kNI + 1;  // pL(a) holds, pL(b) fails
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (pL(mid)) a = mid;
+      else b = mid;
     }
+    kL = a;
+    a = -1;
+    b = kNI + 1;  // pR(a) fails, pR(b) holds
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (pR(mid)) b = mid;
+      else a = mid;
+    }
+    kR = b;  // kNI + 1 = kNB - 1: not in the bracket
   }
+  const long long CuL = kL >= 0 ? (long long)H.cu(kL) : 0, SCL = kL >= 0 ? (long long)H.sc(kL) : 0;
+  const long long CuR = kR <= kNI ? (long long)H.cu(kR) : 0, SCR = kR <= kNI ? (long long)H.sc(kR) : 0;
+  const long long CuC = H.cu(kc), SCC = (long long)H.sc(kc), CuC1 = H.cu(kc + 1), Cu0 = H.cu(0);
+  const long long Cu62 = H.cu(kNI), SC62 = (long long)H.sc(kNI);
   const double q2 = 2.0 * q;
   auto glo = [&](int k, long long Cu) { return q2 * (double)Cu - 2.0 * dC - T + (k >= z0 ? lam : -lam); };
   auto ghi = [&](int k, long long Cu) { return q2 * (double)Cu + 2.0 * dC - T + (k >= z1 ? lam : -lam); };
@@ -500,12 +537,14 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     const bool live = okh && j < m && !dgh && j != (h ? p[1] : p[0]);
     const double ut = h ? unit[1] : unit[0];
     const int64_t kh = h ? kk[1] : kk[0];
+    Prefix H{hist + half * kNB * kBSlots + slot, kBSlots};
+    H.build();  // once for every penalty
     for (int l = 0; l < P.nlam; ++l) {
       double lb = 0.0, ub = 0.0;
       if (live) {
         double2 rg;
         float2 nx;
-        column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
+        column_bounds(H, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
                       (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut,
                       P.lams[l], P.colsum[j], n, sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &rg, &nx);
       } else if (okh && j < m && dgh) {
@@ -551,7 +590,9 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   }
   const double ut = h ? unit[1] : unit[0];
   double lb, ub;
-  column_bounds(hist + half * kNB * kBSlots + slot, kBSlots, ldexp(ut, 21), (double)tlo, (double)thi,
+  Prefix H{hist + half * kNB * kBSlots + slot, kBSlots};
+  H.build();
+  column_bounds(H, ldexp(ut, 21), (double)tlo, (double)thi,
                 (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam, P.colsum[j], n,
                 sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
@@ -578,7 +619,9 @@ __global__ void k_bound_epi(SelParams P, int nsplit) {
   for (int z = 0; z < nsplit; ++z) ec += P.GE[(int64_t)z * P.npiv * m + o];
   const double ut = ldexp(1.0, -P.spow[p]);
   double lb, ub;
-  column_bounds(P.GH + o * kNB, 1, ldexp(ut, 21), (double)g[0], (double)g[1], (double)g[2], ec, P.tq[p] * ut,
+  Prefix H{P.GH + o * kNB, 1};
+  H.build();
+  column_bounds(H, ldexp(ut, 21), (double)g[0], (double)g[1], (double)g[2], ec, P.tq[p] * ut,
                 P.lam, P.colsum[j], P.n, g[3], g[4], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
