@@ -135,6 +135,13 @@ int l1b_argmin(const double* d_obj, int32_t nlam, int64_t npiv, int64_t* d_best_
 int l1b_residual_exact(const double* d_X, int64_t n, int64_t m, const double* d_v, int64_t p,
                        double* d_out, void* d_ws, size_t ws_bytes, void* stream);
 
+/* l1b_residual_exact for `count` candidate lines at once: direction k is
+ * d_V + k*ldv (device), its pivot h_pivots[k]; d_out[k] (device) receives
+ * its exact residual error (NumPy's summation order, bit-identical). */
+int l1b_residual_exact_batch(const double* d_X, int64_t n, int64_t m, const double* d_V, int64_t ldv,
+                             const int64_t* h_pivots, int64_t count, double* d_out, void* d_ws, size_t ws_bytes,
+                             void* stream);
+
 /* subspace.py:22-36 deflate: X <- X - (X w) w^T with w = v / ||v||_2, in
  * place.  d_tmp must hold n + 1 doubles. */
 int l1b_deflate(double* d_X, int64_t n, int64_t m, const double* d_v, double* d_tmp, void* stream);
@@ -177,6 +184,20 @@ int l1b_straggler_records(int64_t n, int64_t m, int64_t npiv, const void* d_ws, 
 int l1b_bound_pivot_list_continue(const double* d_X, int64_t n, int64_t m, double lam, const int64_t* h_pivots,
                                   int64_t npiv, const int64_t* h_from, int64_t from_npiv, double* d_lb,
                                   double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Entry lists (a penalty sweep's survivors, batched): count (pivot, penalty)
+ * entries h_pivots[k], h_lams[k] in one launch.  l1b_bound_entries is one
+ * bounding pass per entry -- from row samples at the entry's penalty, or,
+ * with h_from, continuing from entry h_from[k] of the previous bound call's
+ * list of from_count entries; l1b_fit_entries_seeded is the seeded exact fit
+ * of entries (h_seed[k]: entry of the last bound call).  Same outputs as the
+ * single-penalty calls, per entry. */
+int l1b_bound_entries(const double* d_X, int64_t n, int64_t m, const double* h_lams, const int64_t* h_pivots,
+                      int64_t count, const int64_t* h_from, int64_t from_count, double* d_lb, double* d_ub,
+                      void* d_ws, size_t ws_bytes, void* stream);
+int l1b_fit_entries_seeded(const double* d_X, int64_t n, int64_t m, const double* h_lams, const int64_t* h_pivots,
+                           int64_t count, const int64_t* h_seed, int64_t seed_count, double* d_V, double* d_err,
+                           double* d_pen, double* d_obj, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Exact fit (as l1b_fit_pivot_list, one lambda) of a short pivot list that
  * a preceding l1b_bound_pivot_list call on this workspace bounded: pivot k

@@ -40,6 +40,9 @@ ABI_SYMBOLS = (
     "l1b_bound_pivots_multi",
     "l1b_pivot_breakpoints",
     "l1b_certify_columns",
+    "l1b_bound_entries",
+    "l1b_fit_entries_seeded",
+    "l1b_residual_exact_batch",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -127,6 +130,13 @@ def load() -> ctypes.CDLL:
                                           _vp, _sz, _vp]
     lib.l1b_certify_columns.restype = ctypes.c_int
     lib.l1b_certify_columns.argtypes = [_vp, _i64, _i64, _i64, _vp, ctypes.c_double, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_entries.restype = ctypes.c_int
+    lib.l1b_bound_entries.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_fit_entries_seeded.restype = ctypes.c_int
+    lib.l1b_fit_entries_seeded.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz,
+                                           _vp]
+    lib.l1b_residual_exact_batch.restype = ctypes.c_int
+    lib.l1b_residual_exact_batch.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
         b2 = 0.5f * (r.x + r.y);
       } else {
         sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0], P.delta, &b0,
-                       &b1, &b2, &b3, &b4, MULTI ? P.lams[0] : P.lam, MULTI ? P.lams[P.nlam - 1] : P.lam);
+                       &b1, &b2, &b3, &b4, MULTI ? P.lams[0] : lam_of(P, h ? kk[1] : kk[0]),
+                       MULTI ? P.lams[P.nlam - 1] : lam_of(P, h ? kk[1] : kk[0]));
       }
     }
     float* d = &sbr[half][0][slot];
@@ -593,7 +594,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   Prefix H{hist + half * kNB * kBSlots + slot, kBSlots};
   H.build();
   column_bounds(H, ldexp(ut, 21), (double)tlo, (double)thi,
-                (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, P.lam, P.colsum[j], n,
+                (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, lam_of(P, h ? kk[1] : kk[0]), P.colsum[j], n,
                 sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
@@ -622,7 +623,7 @@ __global__ void k_bound_epi(SelParams P, int nsplit) {
   Prefix H{P.GH + o * kNB, 1};
   H.build();
   column_bounds(H, ldexp(ut, 21), (double)g[0], (double)g[1], (double)g[2], ec, P.tq[p] * ut,
-                P.lam, P.colsum[j], P.n, g[3], g[4], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
+                lam_of(P, kk), P.colsum[j], P.n, g[3], g[4], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
 }

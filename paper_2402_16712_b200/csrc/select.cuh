@@ -85,6 +85,7 @@ struct SelParams {
   unsigned* GH;          // split bound: merged histograms [npiv*m][64]
   double* GE;            // split bound: residual shares [z][npiv*m]
   float* GB;             // split bound: ranges [npiv*m][5]
+  const double* lamk;    // per pivot-list entry penalty (entry lists), or null: lam for all
   const double* lams;    // multi-penalty bound: ascending penalties (device)
   int nlam;
   double* LBm;           // multi-penalty bound: per (penalty, pivot) sums [nlam][npiv]
@@ -94,6 +95,9 @@ struct SelParams {
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {
   return P.pivots ? P.pivots[kk] : P.p_begin + kk * P.p_stride;
 }
+
+// Penalty of pivot-list entry kk (entry lists carry one per entry).
+__device__ __forceinline__ double lam_of(const SelParams& P, int64_t kk) { return P.lamk ? P.lamk[kk] : P.lam; }
 
 // acc += x if p, exactly (x, acc integer-valued): one select of the high
 // word of 1.0 and one DFMA, instead of the add-and-select-both-halves the
@@ -892,7 +896,7 @@ __global__ void __launch_bounds__(kSWarps * 32, 3) k_straggle(SelParams P) {
     Straggler s = P.strag[t];
     const int64_t kk = s.kk, j = s.j, p = pivot_of(P, kk);
     const double Tq = P.tq[p];
-    const double Lsc = ldexp(P.lam, P.spow[p]);
+    const double Lsc = ldexp(lam_of(P, kk), P.spow[p]);
     double G = s.G;
     unsigned long long lo = s.lo, hi = s.hi;
     bool dead = false;
@@ -1113,7 +1117,7 @@ __global__ void __launch_bounds__(kBlkThreads) k_block_solve(SelParams P) {
       }
       continue;
     }
-    const double Tq = P.tq[p], Lsc = ldexp(P.lam, P.spow[p]);
+    const double Tq = P.tq[p], Lsc = ldexp(lam_of(P, kk), P.spow[p]);
     unsigned long long lo = 0, hi = ~0ULL;
     const int64_t sr = P.seeds ? P.seeds[kk] : -1;
     if (sr >= 0) {

@@ -271,6 +271,80 @@ class DeviceFit:
             h = out.cpu().numpy()
         return h[0], h[1], h[2]
 
+    def bound_entries(self, lams, pivots, from_pos=None, from_count: int = 0):
+        """One bounding pass per (pivot, penalty) entry (l1b_bound_entries); with
+        from_pos, continuing from those entries of the last bound call."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
+        fp = None if from_pos is None else np.ascontiguousarray(np.asarray(from_pos, dtype=np.int64))
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, piv.size), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_entries(
+                self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), piv.size,
+                None if fp is None else fp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(from_count),
+                b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+            _lib.check(rc, "l1b_bound_entries")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
+    def fit_entries_seeded(self, lams, pivots, seed, seed_count: int):
+        """Seeded exact fit of (pivot, penalty) entries (l1b_fit_entries_seeded)."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
+        sd = np.ascontiguousarray(np.asarray(seed, dtype=np.int64))
+        k = piv.size
+        with torch.cuda.device(self.device):
+            V = torch.empty((k, self.m), dtype=torch.float64, device=self.device)
+            eo = torch.empty((3, k), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_fit_entries_seeded(
+                self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), k,
+                sd.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(seed_count), V.data_ptr(), eo[0].data_ptr(),
+                eo[1].data_ptr(), eo[2].data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
+        _lib.check(rc, "l1b_fit_entries_seeded")
+        return V, eo[0], eo[1], eo[2]
+
+    def _sweep_winners(self, lam, all_piv, lbm, ubm, uniq, ub_exchange):
+        """Winners of a penalty sweep after one multi-penalty pass: every
+        penalty's survivors are refined and fitted together as one entry list
+        (one launch per cascade level instead of one per penalty)."""
+        L = uniq.size
+        tops, ent_l, ent_k = np.empty(L), [], []
+        for i in range(L):
+            top = float(np.min(ubm[i]))
+            if ub_exchange is not None:
+                top = float(ub_exchange(top))
+            tops[i] = top
+            k = np.nonzero(~(lbm[i] > self._prune_threshold(top)))[0]
+            ent_l.append(np.full(k.size, i, dtype=np.int64))
+            ent_k.append(k)
+        li = np.concatenate(ent_l)           # entry -> penalty index
+        kk = np.concatenate(ent_k)           # entry -> shard pivot position
+        seed, seed_n = None, 0
+        for level in range(REFINE_PASSES + 1):
+            counts = np.bincount(li, minlength=L)
+            if kk.size == 0 or (level > 0 and np.all(counts <= REFINE_MIN)):
+                break
+            lb2, ub2 = self.bound_entries(uniq[li], all_piv[kk], seed, seed_n)
+            np.minimum.at(tops, li, ub2)
+            ok = ~(lb2 > np.array([self._prune_threshold(t) for t in tops])[li])
+            sel = np.nonzero(ok)[0]
+            li, kk, seed, seed_n = li[sel], kk[sel], sel, lb2.size
+        self.last_candidates = int(kk.size)
+        wins = {}
+        if kk.size:
+            V, err, pen, obj = self.fit_entries_seeded(uniq[li], all_piv[kk], seed, seed_n)
+            obj_h = obj.cpu().numpy()
+            ids, groups = [], []
+            for i in range(L):
+                e = np.nonzero(li == i)[0]
+                if e.size:
+                    ids.append(i)
+                    groups.append((float(uniq[i]), all_piv[kk[e]], V[torch.as_tensor(e, device=V.device)], obj_h[e]))
+            wins = dict(zip(ids, self._winners(groups)))
+        return [wins.get(int(np.searchsorted(uniq, x))) for x in lam]
+
     def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
         """One bounding pass for several strictly ascending penalties: lb, ub [L][npiv] (host)."""
         lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
@@ -323,30 +397,57 @@ class DeviceFit:
             bh = b.cpu().numpy()
         return bh[0], bh[1]
 
-    def _winner(self, lam: float, pivots, V, obj_h) -> PivotWinner:
-        """fit.py:98-102 among fitted pivots: re-score the near-minimal ones
-        with the reference's rounding, first strict minimum wins."""
+    def residual_exact_batch(self, V: torch.Tensor, pivots) -> np.ndarray:
+        """residual_exact for the rows of V [C][m] (pivot pivots[k]) in one batch."""
+        piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
+        V = V.contiguous()
+        with torch.cuda.device(self.device):
+            out = torch.empty(piv.size, dtype=torch.float64, device=self.device)
+            _lib.check(self.lib.l1b_residual_exact_batch(
+                self.X.data_ptr(), self.n, self.m, V.data_ptr(), V.stride(0),
+                piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), piv.size, out.data_ptr(), self.ws.data_ptr(),
+                self.ws.numel(), self._s), "l1b_residual_exact_batch")
+            return out.cpu().numpy()
+
+    def _candidates(self, obj_h) -> np.ndarray:
         o = obj_h
-        if np.isnan(o).any():
-            # FittedLine's invariant rejects a NaN objective (core.py:120-124):
-            # only lam=inf with an all-zero pivot column produces one.
-            raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
         best = float(o.min())
         if math.isinf(best):
-            cand = np.nonzero(o == best)[0][:1]
-        else:
-            cand = np.nonzero(o <= best + RESCORE_RTOL * abs(best) + RESCORE_ATOL * self._abs_scale() + 1e-300)[0]
-        win = None
-        for k in cand:  # ascending pivot order
-            p = int(pivots[k])
-            v_dev = V[k]
-            e = self.residual_exact(v_dev, p)
-            vh = v_dev.cpu().numpy().copy()
-            pn = float(np.abs(vh).sum())
-            z = e + float(lam) * pn
-            if win is None or z < win.objective:
-                win = PivotWinner(p, float(lam), vh, e, pn, z)
-        return win
+            return np.nonzero(o == best)[0][:1]
+        return np.nonzero(o <= best + RESCORE_RTOL * abs(best) + RESCORE_ATOL * self._abs_scale() + 1e-300)[0]
+
+    def _winners(self, groups) -> list[PivotWinner]:
+        """fit.py:98-102 for several (lam, pivots, V, obj) groups of fitted
+        pivots: the near-minimal ones of every group are re-scored with the
+        reference's rounding in one batch, the first strict minimum wins."""
+        picks = []
+        for lam, pivots, V, obj_h in groups:
+            if np.isnan(obj_h).any():
+                # FittedLine's invariant rejects a NaN objective (core.py:120-124):
+                # only lam=inf with an all-zero pivot column produces one.
+                raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
+            picks.append(self._candidates(obj_h))
+        rows = torch.cat([V[torch.as_tensor(c, device=V.device)] for (_, _, V, _), c in zip(groups, picks)])
+        pivs = np.concatenate([np.asarray(g[1])[c] for g, c in zip(groups, picks)]).astype(np.int64)
+        errs = self.residual_exact_batch(rows, pivs)
+        vhs = rows.cpu().numpy()
+        out, at = [], 0
+        for (lam, _, _, _), c in zip(groups, picks):
+            win = None
+            for k in range(c.size):  # ascending pivot order
+                vh = vhs[at + k].copy()
+                e = float(errs[at + k])
+                pn = float(np.abs(vh).sum())
+                z = e + float(lam) * pn
+                if win is None or z < win.objective:
+                    win = PivotWinner(int(pivs[at + k]), float(lam), vh, e, pn, z)
+            out.append(win)
+            at += c.size
+        return out
+
+    def _winner(self, lam: float, pivots, V, obj_h) -> PivotWinner:
+        """fit.py:98-102 among fitted pivots (one group of _winners)."""
+        return self._winners([(lam, pivots, V, obj_h)])[0]
 
     def _abs_scale(self) -> float:
         if self._scale is None:
@@ -378,21 +479,16 @@ class DeviceFit:
         if not prune:
             V, err, pen, obj = self.fit_pivots(lam, p_begin, p_stride, npiv, want_v=True)
             obj_h = obj.cpu().numpy()
-            return [self._winner(float(lam[l]), all_piv, V[l], obj_h[l]) for l in range(lam.size)]
+            return self._winners([(float(lam[l]), all_piv, V[l], obj_h[l]) for l in range(lam.size)])
         # several penalties: one bounding pass for all of them (the histogram
         # is penalty-free; each penalty gets its own bounds from it)
         uniq = np.unique(lam[np.isfinite(lam)])
-        multi = None
         if uniq.size > 1 and all(np.isfinite(lam)):
             lbm, ubm = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv)
-            multi = {float(x): (lbm[i], ubm[i]) for i, x in enumerate(uniq)}
+            return self._sweep_winners(lam, all_piv, lbm, ubm, uniq, ub_exchange)
         for l in range(lam.size):
-            if multi is not None:
-                lb, ub = multi[float(lam[l])]
-                fresh = True  # the next level starts from samples at this penalty
-            else:
-                lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
-                fresh = False
+            lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
+            fresh = False
             top = float(np.min(ub))
             if ub_exchange is not None:
                 top = float(ub_exchange(top))  # the best upper bound over every shard

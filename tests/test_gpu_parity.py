@@ -571,3 +571,16 @@ def test_certificates_random_and_at_scale():
     for lam in (1.0, 500.0):
         cert = check_line(d, l1b.fit_line(d, lam))
         assert cert.ok and np.isfinite(cert.slack).sum() == 399
+
+
+def test_residual_exact_batch_equals_single():
+    """l1b_residual_exact_batch == l1b_residual_exact (bit for bit) per candidate."""
+    rng = np.random.default_rng(12)
+    for n, m in ((37, 11), (2000, 300)):
+        X = rng.standard_normal((n, m))
+        eng = DeviceFit(X, max_pivots=4)
+        piv = rng.integers(0, m, size=9)
+        V = torch.from_numpy(rng.standard_normal((9, m))).to(eng.device)
+        got = eng.residual_exact_batch(V, piv)
+        for k in range(9):
+            assert got[k] == eng.residual_exact(V[k], int(piv[k])), (n, m, k)
