@@ -427,10 +427,15 @@ class DeviceFit:
                 # only lam=inf with an all-zero pivot column produces one.
                 raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
             picks.append(self._candidates(obj_h))
-        rows = torch.cat([V[torch.as_tensor(c, device=V.device)] for (_, _, V, _), c in zip(groups, picks)])
         pivs = np.concatenate([np.asarray(g[1])[c] for g, c in zip(groups, picks)]).astype(np.int64)
-        errs = self.residual_exact_batch(rows, pivs)
-        vhs = rows.cpu().numpy()
+        if pivs.size == 1:  # the common case: one candidate, no batching copies
+            row = groups[0][2][int(picks[0][0])]
+            errs = [self.residual_exact(row, int(pivs[0]))]
+            vhs = row.cpu().numpy()[None, :]
+        else:
+            rows = torch.cat([V[torch.as_tensor(c, device=V.device)] for (_, _, V, _), c in zip(groups, picks)])
+            errs = self.residual_exact_batch(rows, pivs)
+            vhs = rows.cpu().numpy()
         out, at = [], 0
         for (lam, _, _, _), c in zip(groups, picks):
             win = None
