@@ -43,6 +43,7 @@ ABI_SYMBOLS = (
     "l1b_bound_entries",
     "l1b_fit_entries_seeded",
     "l1b_residual_exact_batch",
+    "l1b_fit_line",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -137,6 +138,9 @@ def load() -> ctypes.CDLL:
                                            _vp]
     lib.l1b_residual_exact_batch.restype = ctypes.c_int
     lib.l1b_residual_exact_batch.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]
+    lib.l1b_fit_line.restype = ctypes.c_int
+    lib.l1b_fit_line.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, ctypes.c_int32, _vp, _vp, _vp,
+                                 _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

@@ -584,3 +584,22 @@ def test_residual_exact_batch_equals_single():
         got = eng.residual_exact_batch(V, piv)
         for k in range(9):
             assert got[k] == eng.residual_exact(V[k], int(piv[k])), (n, m, k)
+
+
+def test_c_driver_fit_line_equals_unpruned():
+    """l1b_fit_line (the pruned cascade in C++) returns exactly the unpruned winner,
+    forced pruning and auto, and agrees with the Python sweep path."""
+    for seed, (m, n) in enumerate([(60, 900), (40, 5000)]):
+        d, _ = l1b.gen_line_data(m, n, seed=seed + 20, noise_scale=1.0)
+        X = d.values
+        T = float(np.abs(X).sum(axis=0).max())
+        eng = DeviceFit(X)
+        for lam in (0.0, 1.0, 0.2 * T, 2.0 * T):
+            want = eng.fit_line_device(lam, prune=False)
+            for prune in (True, None):
+                got = eng.fit_line_device(lam, prune=prune)
+                assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes()
+                assert (got.error, got.penalty_norm, got.objective) == (want.error, want.penalty_norm, want.objective)
+            sweep = eng.shard_winners([lam, lam + 1.0], prune=True)[0]
+            assert sweep.pivot == want.pivot and sweep.v.tobytes() == want.v.tobytes()
+            assert sweep.objective == want.objective
