@@ -603,3 +603,24 @@ def test_c_driver_fit_line_equals_unpruned():
             sweep = eng.shard_winners([lam, lam + 1.0], prune=True)[0]
             assert sweep.pivot == want.pivot and sweep.v.tobytes() == want.v.tobytes()
             assert sweep.objective == want.objective
+
+
+def test_integration_stub_runs():
+    """The ctypes binding INTEGRATION.md proposes for l1line/gpu.py works as written
+    (library path and FittedLine import adapted) and matches fit_line."""
+    import os
+    import re
+    from conftest import ROOT
+    from paper_2402_16712_b200 import _lib as lib_mod
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(# l1line/gpu.py.*?)```", text, re.S).group(1)
+    code = code.replace("from .core import FittedLine", "from paper_2402_16712_b200.core import FittedLine")
+    code = code.replace('ctypes.CDLL("libl1b200.so")', f"ctypes.CDLL({lib_mod.LIB_PATH!r})")
+    ns = {}
+    exec(compile(code, "INTEGRATION.md", "exec"), ns)
+    d, _ = l1b.gen_line_data(80, 3000, seed=6, noise_scale=1.0)
+    for lam in (1.0, 50.0):
+        got = ns["fit_line"](d, lam)
+        want = l1b.fit_line(d, lam)
+        assert got.preserved == want.preserved and got.v.tobytes() == want.v.tobytes()
+        assert got.objective == want.objective and got.error == want.error
