@@ -185,16 +185,23 @@ int l1b_bound_pivot_list_continue(const double* d_X, int64_t n, int64_t m, doubl
                                   int64_t npiv, const int64_t* h_from, int64_t from_npiv, double* d_lb,
                                   double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
+/* Optional hook of a sharded fit: maps this shard's best upper bound to the
+ * best over all shards (an all-reduce MIN); called once per pruned fit. */
+typedef double (*l1b_ub_exchange_fn)(double top, void* ctx);
+
 /* fit_line (fit.py:88-102) over one pivot shard (p_begin + k p_stride,
  * k < npiv) in one call: bounds every pivot, refines the survivors, fits the
  * rest exactly (seeded) and re-scores the near-minimal ones in NumPy's order;
  * prune = 1 / 0 / -1 (auto: m > 32 and m^2 n >= 2^24).  Outputs the winning
  * pivot, its direction (device d_v[m]) and its error, penalty norm and
  * objective exactly as the reference computes them; *h_candidates (may be
- * NULL) gets the number of pivots fitted exactly.  Synchronises the stream. */
+ * NULL) gets the number of pivots fitted exactly.  With ub_exchange (may be
+ * NULL) the shard prunes against the global best and may keep no pivot:
+ * then *h_pivot = -1.  Synchronises the stream. */
 int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
-                 int64_t npiv, int32_t prune, int64_t* h_pivot, double* d_v, double* h_err, double* h_pen,
-                 double* h_obj, int64_t* h_candidates, void* d_ws, size_t ws_bytes, void* stream);
+                 int64_t npiv, int32_t prune, l1b_ub_exchange_fn ub_exchange, void* exchange_ctx, int64_t* h_pivot,
+                 double* d_v, double* h_err, double* h_pen, double* h_obj, int64_t* h_candidates, void* d_ws,
+                 size_t ws_bytes, void* stream);
 
 /* Entry lists (a penalty sweep's survivors, batched): count (pivot, penalty)
  * entries h_pivots[k], h_lams[k] in one launch.  l1b_bound_entries is one

@@ -48,6 +48,9 @@ ABI_SYMBOLS = (
     "l1b_atoms_probe",
 )
 
+# double (*)(double top, void* ctx): the sharded fit's upper-bound exchange hook
+UB_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+
 L1B_OK = 0
 L1B_EINVAL = -1
 L1B_ECUDA = -2
@@ -139,8 +142,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_residual_exact_batch.restype = ctypes.c_int
     lib.l1b_residual_exact_batch.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]
     lib.l1b_fit_line.restype = ctypes.c_int
-    lib.l1b_fit_line.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, ctypes.c_int32, _vp, _vp, _vp,
-                                 _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_fit_line.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, ctypes.c_int32, UB_EXCHANGE_FN,
+                                 _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

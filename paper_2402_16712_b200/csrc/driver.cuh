@@ -45,8 +45,9 @@ double np_pairwise(const double* a, int64_t n) {
 extern "C" {
 
 int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
-                 int64_t npiv, int32_t prune, int64_t* h_pivot, double* d_v, double* h_err, double* h_pen,
-                 double* h_obj, int64_t* h_candidates, void* d_ws, size_t ws_bytes, void* stream) {
+                 int64_t npiv, int32_t prune, l1b_ub_exchange_fn ub_exchange, void* exchange_ctx, int64_t* h_pivot,
+                 double* d_v, double* h_err, double* h_pen, double* h_obj, int64_t* h_candidates, void* d_ws,
+                 size_t ws_bytes, void* stream) {
   if (!d_X || !h_pivot || !d_v || !h_err || !h_pen || !h_obj || n < 1 || m < 2 || npiv < 1 || !(lam >= 0.0))
     return L1B_EINVAL;
   if (p_stride < 1 || p_begin < 0 || p_begin + (npiv - 1) * p_stride >= m) return L1B_EINVAL;
@@ -89,6 +90,7 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
       return L1B_ECUDA;
     double top = INFINITY;
     for (double u : ub) top = std::min(top, u);  // NaN never wins std::min here
+    if (ub_exchange) top = ub_exchange(top, exchange_ctx);  // the best upper bound over every shard
     std::vector<int64_t> keep;
     for (int64_t k = 0; k < npiv; ++k)
       if (!(lb[k] > thr(top))) keep.push_back(k);  // NaN-safe: keep unless provably worse
@@ -119,7 +121,11 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
     }
     cand_piv = list;
     nfit = (int64_t)cand_piv.size();
-    if (nfit == 0) return L1B_EINTERNAL;  // cannot happen: the best upper bound's pivot always survives
+    if (nfit == 0) {  // another shard holds a pivot provably better than all of ours
+      *h_pivot = -1;
+      if (h_candidates) *h_candidates = 0;
+      return L1B_OK;
+    }
     st = fit_impl(d_X, n, m, &lam, 1, 0, 1, cand_piv.data(), nfit, false, nullptr, d_err, d_pen, d_obj, nullptr,
                   nullptr, d_ws, ws_bytes, stream, 1, seed.data(), seed_n);
   } else {

@@ -479,9 +479,9 @@ class DeviceFit:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         all_piv = p_begin + p_stride * np.arange(npiv, dtype=np.int64)
         out = []
-        if lam.size == 1 and ub_exchange is None:
-            # one penalty, one shard: the whole cascade in one C call (no Python round trips)
-            return [self.fit_line_device(float(lam[0]), p_begin, p_stride, npiv, prune)]
+        if lam.size == 1:
+            # one penalty: the whole cascade in one C call (no Python round trips)
+            return [self.fit_line_device(float(lam[0]), p_begin, p_stride, npiv, prune, ub_exchange)]
         if prune is None:
             prune = self.auto_prune()
         if not prune:
@@ -528,23 +528,33 @@ class DeviceFit:
         return out
 
     def fit_line_device(self, lam: float, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None,
-                        prune: bool | None = None) -> PivotWinner:
-        """shard_winners for one penalty via l1b_fit_line (the same cascade in C++)."""
+                        prune: bool | None = None, ub_exchange=None) -> PivotWinner | None:
+        """shard_winners for one penalty via l1b_fit_line (the same cascade in C++).
+
+        ``ub_exchange(top) -> global top`` is handed to the library as its
+        exchange hook (called once, only when pruning; a shard whose pivots
+        are all beaten returns None)."""
         if npiv is None:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         piv, cand = ctypes.c_int64(), ctypes.c_int64()
         err, pen, obj = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        hook = _lib.UB_EXCHANGE_FN(0) if ub_exchange is None else \
+            _lib.UB_EXCHANGE_FN(lambda top, ctx: float(ub_exchange(top)))
+        if ub_exchange is not None and prune is None:
+            prune = self.auto_prune()  # every rank must take the same path
         with torch.cuda.device(self.device):
             v = torch.empty(self.m, dtype=torch.float64, device=self.device)
             rc = self.lib.l1b_fit_line(self.X.data_ptr(), self.n, self.m, float(lam), p_begin, p_stride, npiv,
-                                       -1 if prune is None else int(bool(prune)), ctypes.byref(piv), v.data_ptr(),
-                                       ctypes.byref(err), ctypes.byref(pen), ctypes.byref(obj), ctypes.byref(cand),
-                                       self.ws.data_ptr(), self.ws.numel(), self._s)
+                                       -1 if prune is None else int(bool(prune)), hook, None, ctypes.byref(piv),
+                                       v.data_ptr(), ctypes.byref(err), ctypes.byref(pen), ctypes.byref(obj),
+                                       ctypes.byref(cand), self.ws.data_ptr(), self.ws.numel(), self._s)
             if rc == _lib.L1B_EINVAL and math.isinf(lam):
                 raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
             _lib.check(rc, "l1b_fit_line")
             vh = v.cpu().numpy()
         self.last_candidates = int(cand.value)
+        if piv.value < 0:
+            return None
         return PivotWinner(int(piv.value), float(lam), vh, float(err.value), float(pen.value), float(obj.value))
 
     def auto_prune(self) -> bool:
