@@ -33,6 +33,7 @@ extern "C" {
 #define L1B_ECUDA -2    /* CUDA launch or runtime failure                          */
 #define L1B_ENOMEM -3   /* workspace too small                                     */
 #define L1B_EINTERNAL -4
+#define L1B_EFALLBACK -5  /* l1b_csv_read: the file needs the reference's general CSV rules    */
 
 /* Human-readable text for a status code. */
 const char* l1b_status_string(int status);
@@ -254,6 +255,18 @@ uint64_t l1b_kernel_launches(void);
  * with CUDA events to measure the FP64 peak the roofline is quoted against.
  * d_out: one device double (written only to keep the chains alive). */
 int l1b_dfma_probe(int64_t iters, int32_t blocks, int32_t threads, double* d_out, void* stream);
+
+/* read_matrix (io.py:46-85) for plain numeric CSV files, natively and in
+ * parallel (threads <= 0: all cores): *out_values (row-major n x m,
+ * malloc'd; free with l1b_csv_free) holds exactly the doubles float()
+ * parses.  Returns L1B_EFALLBACK for quotes, underscores, non-ASCII bytes,
+ * lone CRs, and for every malformed file (ragged rows, non-numeric or
+ * non-finite cells, no data): the caller then applies the reference's rules
+ * (and its exact error messages).  With has_header, *out_header (malloc'd,
+ * may be NULL) is the header line. */
+int l1b_csv_read(const char* path, int32_t has_header, int32_t threads, double** out_values, int64_t* out_n,
+                 int64_t* out_m, char** out_header);
+void l1b_csv_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -17,9 +17,10 @@ _API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspa
         "residual_error", "resolve_threads")
 _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions")
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
+_IO = ("read_matrix", "write_matrix", "CsvParseError")
 
 __all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "SubspaceFit", "gen_line_data",
-           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, "__version__"]
+           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, "__version__"]
 
 
 def __getattr__(name):
@@ -33,6 +34,9 @@ def __getattr__(name):
     if name in _CERT:
         from . import certify
         return getattr(certify, name)
+    if name in _IO:
+        from . import io
+        return getattr(io, name)
     if name == "use_gpu":
         from .integration import use_gpu
         return use_gpu

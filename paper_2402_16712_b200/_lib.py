@@ -44,6 +44,8 @@ ABI_SYMBOLS = (
     "l1b_fit_entries_seeded",
     "l1b_residual_exact_batch",
     "l1b_fit_line",
+    "l1b_csv_read",
+    "l1b_csv_free",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -55,6 +57,7 @@ L1B_OK = 0
 L1B_EINVAL = -1
 L1B_ECUDA = -2
 L1B_ENOMEM = -3
+L1B_EFALLBACK = -5
 L1B_EINTERNAL = -4
 
 _lib = None
@@ -144,6 +147,12 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_line.restype = ctypes.c_int
     lib.l1b_fit_line.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, ctypes.c_int32, UB_EXCHANGE_FN,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_csv_read.restype = ctypes.c_int
+    lib.l1b_csv_read.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32,
+                                 ctypes.POINTER(ctypes.POINTER(ctypes.c_double)), ctypes.POINTER(ctypes.c_int64),
+                                 ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_char_p)]
+    lib.l1b_csv_free.restype = None
+    lib.l1b_csv_free.argtypes = [_vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

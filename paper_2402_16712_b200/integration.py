@@ -59,14 +59,21 @@ def use_gpu(module: str = "l1line") -> None:
                   for p, pb in sols.pivots.items()}
         return grid, rp.PivotSolutions(data, pivots, sols.degenerate)
 
+    def read_matrix(path, has_header=False):
+        # the native CSV reader, returning the reference's own DataMatrix
+        from . import io
+        d = io.read_matrix(path, has_header)
+        return ref_core.DataMatrix(d.values, column_names=d.column_names)
+
     targets = {
+        "read_matrix": read_matrix,
         "fit_line": fit_line,
         "fit_for_pivot": fit_for_pivot,
         "fit_subspace": fit_subspace,
         "pivot_breakpoints": pivot_breakpoints,
         "major_breakpoints": major_breakpoints,
     }
-    for modname in ("", ".fit", ".subspace", ".oracle", ".cli", ".path"):
+    for modname in ("", ".fit", ".subspace", ".oracle", ".cli", ".path", ".io"):
         try:
             mod = importlib.import_module(module + modname)
         except ImportError:

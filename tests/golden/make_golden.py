@@ -208,9 +208,65 @@ def breakpoint_cases():
     np.savez_compressed(os.path.join(OUT, "breakpoints.npz"), **out)
 
 
+CSV_CASES = {
+    "plain": "1.5,2,3\n4,5e-3,-6\n",
+    "header": "a, b ,c\n1,2,3\n4,5,6\n",
+    "crlf_blank": "1,2\r\n\r\n , \r\n3,4\r\n\r\n",
+    "plus_space": " +1.25 ,\t-2.5\n3e2 , .5\n",
+    "quoted": '"1.5",2\n3,"4e1"\n',
+    "underscore": "1_000,2\n3,4\n",
+    "ragged": "1,2,3\n4,5\n",
+    "nonnumeric": "1,2\n3,abc\n",
+    "empty_cell": "1,,3\n4,5,6\n",
+    "nan": "1,2\nnan,4\n",
+    "inf": "1,2\n3,-inf\n",
+    "overflow": "1,2\n3,1e400\n",
+    "underflow": "1e-400,2\n3,4.9e-324\n",
+    "no_data": "\n\n",
+    "header_only": "x,y\n",
+    "header_mismatch": "x,y,z\n1,2\n",
+    "one_col": "1\n2\n",
+    "exp_forms": "1E5,2.E-3\n-0,0.0\n",
+    "long_digits": "0.1000000000000000055511151231257827,3.141592653589793238462643383279\n2.718281828459045235360287,1\n",
+    "unicode": "1,\u0663\n2,3\n",
+}
+
+
+def csv_cases():
+    """io.read_matrix / write_matrix (io.py:46-98) on edge-case files: the
+    files under csv/ and the reference's outcome for each (values as hex, or
+    the exception with its row and column)."""
+    import json
+
+    from l1line import io as rio
+    out = os.path.join(OUT, "csv")
+    os.makedirs(out, exist_ok=True)
+    exp = {}
+    for name, text in CSV_CASES.items():
+        p = os.path.join(out, name + ".csv")
+        with open(p, "w", newline="", encoding="utf-8") as f:
+            f.write(text)
+        for hh in (False, True):
+            key = f"{name}|{int(hh)}"
+            try:
+                d = rio.read_matrix(p, has_header=hh)
+                exp[key] = {"ok": True, "shape": list(d.values.shape),
+                            "hex": [float(x).hex() for x in d.values.ravel()],
+                            "names": list(d.column_names) if d.column_names else None}
+            except rio.CsvParseError as e:
+                exp[key] = {"ok": False, "type": "CsvParseError", "msg": str(e), "row": e.row, "col": e.column}
+            except ValueError as e:
+                exp[key] = {"ok": False, "type": "ValueError", "msg": str(e)}
+    d, _ = l1line.gen_line_data(7, 5, seed=3, noise_scale=1.0)
+    rio.write_matrix(d, os.path.join(out, "written.csv"), header=True)
+    np.save(os.path.join(out, "written_X.npy"), d.values)
+    with open(os.path.join(out, "expected.json"), "w") as f:
+        json.dump(exp, f, indent=0, sort_keys=True)
+
+
 if __name__ == "__main__":
     want = set(sys.argv[1:])
-    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases):
+    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases, csv_cases):
         if not want or f.__name__ in want:
             f()
     for f in sorted(os.listdir(OUT)):
