@@ -319,30 +319,45 @@ class DeviceFit:
             k = np.nonzero(~(lbm[i] > self._prune_threshold(top)))[0]
             ent_l.append(np.full(k.size, i, dtype=np.int64))
             ent_k.append(k)
-        li = np.concatenate(ent_l)           # entry -> penalty index
-        kk = np.concatenate(ent_k)           # entry -> shard pivot position
-        seed, seed_n = None, 0
-        for level in range(REFINE_PASSES + 1):
-            counts = np.bincount(li, minlength=L)
-            if kk.size == 0 or (level > 0 and np.all(counts <= REFINE_MIN)):
-                break
-            lb2, ub2 = self.bound_entries(uniq[li], all_piv[kk], seed, seed_n)
-            np.minimum.at(tops, li, ub2)
-            ok = ~(lb2 > np.array([self._prune_threshold(t) for t in tops])[li])
-            sel = np.nonzero(ok)[0]
-            li, kk, seed, seed_n = li[sel], kk[sel], sel, lb2.size
-        self.last_candidates = int(kk.size)
+        # entry lists are bounded by the workspace's pivot capacity: penalties
+        # go in batches whose survivors fit
+        batches, cur, size = [], [], 0
+        for i in range(L):
+            c = ent_k[i].size
+            if cur and size + c > self.max_pivots:
+                batches.append(cur)
+                cur, size = [], 0
+            cur.append(i)
+            size += c
+        if cur:
+            batches.append(cur)
         wins = {}
-        if kk.size:
-            V, err, pen, obj = self.fit_entries_seeded(uniq[li], all_piv[kk], seed, seed_n)
-            obj_h = obj.cpu().numpy()
-            ids, groups = [], []
-            for i in range(L):
-                e = np.nonzero(li == i)[0]
-                if e.size:
-                    ids.append(i)
-                    groups.append((float(uniq[i]), all_piv[kk[e]], V[torch.as_tensor(e, device=V.device)], obj_h[e]))
-            wins = dict(zip(ids, self._winners(groups)))
+        self.last_candidates = 0
+        for bl in batches:
+            li = np.concatenate([ent_l[i] for i in bl])  # entry -> penalty index
+            kk = np.concatenate([ent_k[i] for i in bl])  # entry -> shard pivot position
+            seed, seed_n = None, 0
+            for level in range(REFINE_PASSES + 1):
+                counts = np.bincount(li, minlength=L)
+                if kk.size == 0 or (level > 0 and np.all(counts <= REFINE_MIN)):
+                    break
+                lb2, ub2 = self.bound_entries(uniq[li], all_piv[kk], seed, seed_n)
+                np.minimum.at(tops, li, ub2)
+                ok = ~(lb2 > np.array([self._prune_threshold(t) for t in tops])[li])
+                sel = np.nonzero(ok)[0]
+                li, kk, seed, seed_n = li[sel], kk[sel], sel, lb2.size
+            self.last_candidates += int(kk.size)
+            if kk.size:
+                V, err, pen, obj = self.fit_entries_seeded(uniq[li], all_piv[kk], seed, seed_n)
+                obj_h = obj.cpu().numpy()
+                ids, groups = [], []
+                for i in bl:
+                    e = np.nonzero(li == i)[0]
+                    if e.size:
+                        ids.append(i)
+                        groups.append((float(uniq[i]), all_piv[kk[e]], V[torch.as_tensor(e, device=V.device)],
+                                       obj_h[e]))
+                wins.update(zip(ids, self._winners(groups)))
         return [wins.get(int(np.searchsorted(uniq, x))) for x in lam]
 
     def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):

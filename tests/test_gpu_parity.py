@@ -624,3 +624,23 @@ def test_integration_stub_runs():
         want = l1b.fit_line(d, lam)
         assert got.preserved == want.preserved and got.v.tobytes() == want.v.tobytes()
         assert got.objective == want.objective and got.error == want.error
+
+
+def test_pruned_paths_random_stress():
+    """A short run of tools/stress_prune.py's check (pruned == unpruned, bit for
+    bit) over Gaussian, Cauchy, tied, sparse and badly scaled data, including
+    sweeps whose survivors exceed the workspace's pivot capacity."""
+    rng = np.random.default_rng(99)
+    for t in range(12):
+        m, n = int(rng.integers(34, 90)), int(rng.integers(50, 1500))
+        X = [rng.standard_normal((n, m)), rng.standard_cauchy((n, m)), np.round(rng.uniform(-5, 5, (n, m))),
+             rng.standard_normal((n, m)) * np.exp(rng.uniform(-8, 8, (1, m)))][t % 4]
+        T = float(np.abs(X).sum(axis=0).max())
+        lams = [0.0, 1.0, 0.1 * T, 0.8 * T]
+        eng = DeviceFit(X)
+        full = eng.shard_winners(lams, prune=False)
+        for lam, want in zip(lams, full):
+            got = eng.fit_line_device(lam, prune=True)
+            assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes() and got.objective == want.objective
+        for a, b in zip(eng.shard_winners(lams, prune=True), full):
+            assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes() and a.objective == b.objective
