@@ -1139,6 +1139,60 @@ __global__ void __launch_bounds__(kBlkThreads) k_block_solve(SelParams P) {
     bool ok = false;
     for (int round = 0; round < 64 && !ok; ++round) {
       const bool needG = G < 0.0;
+      if (lo == hi && !needG) {
+        // one key left (heavy exact ties): the value is that key; only a zero
+        // needs the crossing row itself (its sign), found by an in-order
+        // prefix walk over the tied rows, 256 rows at a time
+        if (lo != kZeroKey) {
+          v = key64_inv(lo);
+          ok = true;
+          break;
+        }
+        double wb = 0.0;
+        for (int64_t i = tid; i < n; i += kBlkThreads) {
+          double w;
+          const unsigned long long k = row_key(i, &w);
+          if (w != 0.0 && k < lo) wb += w;
+        }
+        double cum = block_sum(wb, red);
+        int hit_row = -1;
+        for (int64_t i0 = 0; i0 < n && hit_row < 0; i0 += kBlkThreads) {
+          const int64_t i = i0 + tid;
+          double x = 0.0;
+          if (i < n) {
+            double w;
+            const unsigned long long k = row_key(i, &w);
+            x = (w != 0.0 && k == lo) ? w : 0.0;
+          }
+          // inclusive block scan of x in row order
+          double y = x;
+          for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, y, o);
+            if ((tid & 31) >= o) y += t;
+          }
+          __syncthreads();
+          if ((tid & 31) == 31) red[tid >> 5] = y;
+          __syncthreads();
+          double off = 0.0, tot = 0.0;
+          for (int k = 0; k < kBlkThreads / 32; ++k) {
+            off += k < (tid >> 5) ? red[k] : 0.0;
+            tot += red[k];
+          }
+          const bool hit = x > 0.0 && cum + off + y > G;
+          if (tid == 0) cnt_s = 0x7fffffff;
+          __syncthreads();
+          if (hit) atomicMin(&cnt_s, tid);
+          __syncthreads();
+          if (cnt_s != 0x7fffffff) hit_row = (int)(i0 + cnt_s);
+          cum += tot;
+          __syncthreads();
+        }
+        if (hit_row >= 0) {
+          v = __ddiv_rn(xc[hit_row], pb[hit_row]);
+          ok = true;
+        }
+        break;
+      }
       if (tid == 0) cnt_s = 0;
       __syncthreads();
       double wbl = 0.0, wneg = 0.0;

@@ -644,3 +644,26 @@ def test_pruned_paths_random_stress():
             assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes() and got.objective == want.objective
         for a, b in zip(eng.shard_winners(lams, prune=True), full):
             assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes() and a.objective == b.objective
+
+
+def test_block_solver_heavy_ties_and_signed_zero():
+    """Tall data (block-per-problem exact solver): a crossing key shared by
+    thousands of rows (grid data) and a column whose weighted median is a
+    zero ratio (its sign from the crossing row) -- the case a random stress
+    run found; pruned == unpruned bit for bit."""
+    rng = np.random.default_rng(31)
+    n, m = 9000, 36
+    X = np.round(rng.standard_normal((n, m)) * 4) / 4
+    X[rng.random(n) < 0.7, 5] = 0.0
+    X[rng.random(n) < 0.2, 5] = -0.0
+    X[:, 9] = 0.0
+    eng = DeviceFit(X)
+    for lam in (0.0, 1.0, 50.0):
+        want = eng.fit_line_device(lam, prune=False)
+        got = eng.fit_line_device(lam, prune=True)
+        assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes() and got.objective == want.objective
+        for p in (0, 5):  # every column of two pivots through the seeded block solver
+            lb, ub = eng.bound_pivot_list(lam, [p], passes=3)
+            V, _, _, _ = eng.fit_pivot_list_seeded(lam, [p], [0], 1)
+            V0, _, _, _ = eng.fit_pivot_list([lam], [p])
+            assert V[0, 0].cpu().numpy().tobytes() == V0[0, 0].cpu().numpy().tobytes()
