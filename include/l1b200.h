@@ -268,6 +268,19 @@ int l1b_csv_read(const char* path, int32_t has_header, int32_t threads, double**
                  int64_t* out_m, char** out_header);
 void l1b_csv_free(void* p);
 
+/* Algorithm 3 (path.py:166-277, merge_path) on the host, bit-identical to
+ * the reference: X host row-major n x m; the grid lambdas[K]; usable pivots
+ * piv[np_] and degenerate pivots deg[nd], both ascending; breakpoint events
+ * (pivot ev_p, target ev_t, value ev_v) grouped by snapped grid index
+ * (ev_off[K+1]) in the reference's insertion order.  Writes up to cap path
+ * segments (o_lo, o_hi, o_piv, o_v [cap][m], o_err, o_pen, o_obj, o_zlo,
+ * o_zhi) and *count; L1B_ENOMEM (with *count set) when cap is short. */
+int l1b_merge_path(const double* X, int64_t n, int64_t m, const double* lambdas, int64_t K, const int64_t* piv,
+                   int64_t np_, const int64_t* deg, int64_t nd, const int64_t* ev_off, const int64_t* ev_p,
+                   const int64_t* ev_t, const double* ev_v, int64_t cap, double* o_lo, double* o_hi,
+                   int64_t* o_piv, double* o_v, double* o_err, double* o_pen, double* o_obj, double* o_zlo,
+                   double* o_zhi, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

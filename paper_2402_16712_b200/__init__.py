@@ -8,18 +8,19 @@ GPU (types, data generation); the first fit loads ``csrc/libl1b200.so`` and
 requires a CUDA device -- there is no CPU fallback.
 """
 
-from .core import DataMatrix, EmptyPivotError, FittedLine, SubspaceFit
+from .core import DataMatrix, EmptyPivotError, FittedLine, PathSegment, SolutionPath, SubspaceFit
 from .datagen import gen_line_data, gen_outlier_data, laplace
 
 __version__ = "0.1.0"
 
 _API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
         "residual_error", "resolve_threads")
-_PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions")
+_PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions", "merge_path",
+         "solution_path")
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
 _IO = ("read_matrix", "write_matrix", "CsvParseError")
 
-__all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "SubspaceFit", "gen_line_data",
+__all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "PathSegment", "SolutionPath", "SubspaceFit", "gen_line_data",
            "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, "__version__"]
 
 

@@ -46,6 +46,7 @@ ABI_SYMBOLS = (
     "l1b_fit_line",
     "l1b_csv_read",
     "l1b_csv_free",
+    "l1b_merge_path",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
 )
@@ -153,6 +154,9 @@ def load() -> ctypes.CDLL:
                                  ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_char_p)]
     lib.l1b_csv_free.restype = None
     lib.l1b_csv_free.argtypes = [_vp]
+    lib.l1b_merge_path.restype = ctypes.c_int
+    lib.l1b_merge_path.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _i64,
+                                   _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     lib.l1b_last_bound_ms.restype = ctypes.c_int
     lib.l1b_last_bound_ms.argtypes = [ctypes.POINTER(ctypes.c_float)]
     lib.l1b_atoms_probe.restype = ctypes.c_int

@@ -15,7 +15,10 @@ right end is the column's death weight.  The device
 the stable sort of every column and the sequential prefix sums -- the
 reference's 84 % -- bit for bit; this module keeps the
 live runs and builds the same entry tuples.  The envelope merge
-(Algorithm 3, ``merge_path``) is not ported.
+(Algorithm 3, ``merge_path``, path.py:166-277) runs natively too
+(``l1b_merge_path``, ``csrc/merge.inc``): the same operations in the same
+order in C++, so the path's breakpoints, lines and objectives are
+bit-identical to the reference's.
 """
 
 from __future__ import annotations
@@ -26,10 +29,11 @@ from dataclasses import dataclass
 import numpy as np
 
 from .api import _as_data, resolve_threads
-from .core import DataMatrix, EmptyPivotError
+from .core import DataMatrix, EmptyPivotError, FittedLine, PathSegment, SolutionPath
 from .engine import DeviceFit
 
-__all__ = ["PivotBreakpoints", "PivotSolutions", "pivot_breakpoints", "major_breakpoints", "DEDUP_TOL"]
+__all__ = ["PivotBreakpoints", "PivotSolutions", "pivot_breakpoints", "major_breakpoints", "merge_path",
+           "solution_path", "DEDUP_TOL"]
 
 DEDUP_TOL = 1e-9  # path.py:34: breakpoints closer than this (absolute) are one
 
@@ -154,3 +158,77 @@ def major_breakpoints(data, threads: int | None = None) -> tuple[np.ndarray, Piv
         except EmptyPivotError:
             degenerate.append(p)
     return _dedup(np.concatenate(weights)), PivotSolutions(d, pivots, tuple(degenerate))
+
+
+def _snap_indices(lambdas: np.ndarray, bps: np.ndarray) -> np.ndarray:
+    """path.py:157-163 for an array of breakpoints."""
+    idx = np.searchsorted(lambdas, bps)
+    K = lambdas.size
+    ic = np.minimum(idx, K - 1)
+    here = (idx < K) & (np.abs(lambdas[ic] - bps) <= DEDUP_TOL)
+    im = np.maximum(idx - 1, 0)
+    left = (idx > 0) & (np.abs(lambdas[im] - bps) <= DEDUP_TOL)
+    if not np.all(here | left):
+        raise AssertionError("a breakpoint is missing from the weight grid")
+    return np.where(here, idx, idx - 1)
+
+
+def merge_path(lambdas, solutions: PivotSolutions, data) -> SolutionPath:
+    """Lower envelope of the per-pivot objectives across the weight grid
+    (path.py:166-277), in C++ (``l1b_merge_path``)."""
+    import ctypes
+
+    from . import _lib
+    d = _as_data(data)
+    X = np.ascontiguousarray(d.values, dtype=np.float64)
+    lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64))
+    piv = np.asarray(sorted(solutions.pivots), dtype=np.int64)
+    deg = np.asarray(sorted(solutions.degenerate), dtype=np.int64)
+    ep, et, ev, eb = [], [], [], []
+    for p in piv.tolist():  # the reference's event order: pivot, target, entry
+        for t, entries in solutions.pivots[p].entries.items():
+            for bp, val in entries:
+                ep.append(p)
+                et.append(t)
+                ev.append(val)
+                eb.append(bp)
+    k = _snap_indices(lam, np.asarray(eb, dtype=np.float64)) if eb else np.zeros(0, dtype=np.int64)
+    order = np.argsort(k, kind="stable")  # grouped by grid index, insertion order kept
+    ep = np.ascontiguousarray(np.asarray(ep, dtype=np.int64)[order])
+    et = np.ascontiguousarray(np.asarray(et, dtype=np.int64)[order])
+    ev = np.ascontiguousarray(np.asarray(ev, dtype=np.float64)[order])
+    off = np.ascontiguousarray(np.searchsorted(k[order], np.arange(lam.size + 1)).astype(np.int64))
+    lib = _lib.load()
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    pd = ctypes.POINTER(ctypes.c_double)
+    cap = 64
+    while True:
+        o = {nm: np.empty(cap) for nm in ("lo", "hi", "err", "pen", "obj", "zlo", "zhi")}
+        opiv = np.empty(cap, dtype=np.int64)
+        ov = np.empty((cap, d.m))
+        cnt = ctypes.c_int64()
+        rc = lib.l1b_merge_path(
+            X.ctypes.data_as(pd), d.n, d.m, lam.ctypes.data_as(pd), lam.size, piv.ctypes.data_as(p64), piv.size,
+            deg.ctypes.data_as(p64), deg.size, off.ctypes.data_as(p64), ep.ctypes.data_as(p64),
+            et.ctypes.data_as(p64), ev.ctypes.data_as(pd), cap, o["lo"].ctypes.data_as(pd),
+            o["hi"].ctypes.data_as(pd), opiv.ctypes.data_as(p64), ov.ctypes.data_as(pd), o["err"].ctypes.data_as(pd),
+            o["pen"].ctypes.data_as(pd), o["obj"].ctypes.data_as(pd), o["zlo"].ctypes.data_as(pd),
+            o["zhi"].ctypes.data_as(pd), ctypes.byref(cnt))
+        if rc == _lib.L1B_ENOMEM and cnt.value > cap:
+            cap = int(cnt.value)
+            continue
+        _lib.check(rc, "l1b_merge_path")
+        break
+    segs = []
+    for s_ in range(int(cnt.value)):
+        line = FittedLine(v=ov[s_].copy(), preserved=int(opiv[s_]), lam=float(o["lo"][s_]), error=float(o["err"][s_]),
+                          penalty_norm=float(o["pen"][s_]), objective=float(o["obj"][s_]))
+        segs.append(PathSegment(lambda_lo=float(o["lo"][s_]), lambda_hi=float(o["hi"][s_]), line=line,
+                                z_lo=float(o["zlo"][s_]), z_hi=float(o["zhi"][s_])))
+    return SolutionPath(tuple(segs))
+
+
+def solution_path(data, threads: int | None = None) -> SolutionPath:
+    """Breakpoint grid plus envelope merge in one call (path.py:280-283)."""
+    lambdas, sols = major_breakpoints(data, threads)
+    return merge_path(lambdas, sols, data)

@@ -208,6 +208,27 @@ def breakpoint_cases():
     np.savez_compressed(os.path.join(OUT, "breakpoints.npz"), **out)
 
 
+def path_cases():
+    """Algorithm 3 (path.py:166-283): the reference's solution_path on the
+    breakpoint cases, segment by segment."""
+    g = np.load(os.path.join(OUT, "breakpoints.npz"))
+    out = {}
+    for name in g["names"]:
+        X = g[f"{name}_X"]
+        path = l1line.solution_path(l1line.DataMatrix(X), threads=1)
+        segs = path.segments
+        out[f"{name}_lo"] = np.asarray([sg.lambda_lo for sg in segs])
+        out[f"{name}_hi"] = np.asarray([sg.lambda_hi for sg in segs])
+        out[f"{name}_zlo"] = np.asarray([sg.z_lo for sg in segs])
+        out[f"{name}_zhi"] = np.asarray([sg.z_hi for sg in segs])
+        out[f"{name}_piv"] = np.asarray([sg.line.preserved for sg in segs], dtype=np.int64)
+        out[f"{name}_v"] = np.asarray([sg.line.v for sg in segs])
+        out[f"{name}_err"] = np.asarray([sg.line.error for sg in segs])
+        out[f"{name}_pen"] = np.asarray([sg.line.penalty_norm for sg in segs])
+        out[f"{name}_obj"] = np.asarray([sg.line.objective for sg in segs])
+    np.savez_compressed(os.path.join(OUT, "paths.npz"), names=g["names"], **out)
+
+
 CSV_CASES = {
     "plain": "1.5,2,3\n4,5e-3,-6\n",
     "header": "a, b ,c\n1,2,3\n4,5,6\n",
@@ -266,7 +287,7 @@ def csv_cases():
 
 if __name__ == "__main__":
     want = set(sys.argv[1:])
-    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases, csv_cases):
+    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases, path_cases, csv_cases):
         if not want or f.__name__ in want:
             f()
     for f in sorted(os.listdir(OUT)):

@@ -667,3 +667,18 @@ def test_block_solver_heavy_ties_and_signed_zero():
             V, _, _, _ = eng.fit_pivot_list_seeded(lam, [p], [0], 1)
             V0, _, _, _ = eng.fit_pivot_list([lam], [p])
             assert V[0, 0].cpu().numpy().tobytes() == V0[0, 0].cpu().numpy().tobytes()
+
+
+def test_solution_path_matches_reference():
+    """solution_path = device breakpoints (k_breakpoints) + native merge: the
+    reference's paths (tests/golden/paths.npz) bit for bit."""
+    from paper_2402_16712_b200 import solution_path
+    bp = load_golden("breakpoints.npz")
+    g = load_golden("paths.npz")
+    for name in bp["names"]:
+        path = solution_path(bp[f"{name}_X"])
+        segs = path.segments
+        assert np.asarray([s.line.preserved for s in segs]).tolist() == g[f"{name}_piv"].tolist(), name
+        assert np.asarray([s.lambda_lo for s in segs]).tobytes() == g[f"{name}_lo"].tobytes(), name
+        assert np.asarray([s.line.v for s in segs]).tobytes() == g[f"{name}_v"].tobytes(), name
+        assert np.asarray([s.line.objective for s in segs]).tobytes() == g[f"{name}_obj"].tobytes(), name
