@@ -65,7 +65,22 @@ def use_gpu(module: str = "l1line") -> None:
         d = io.read_matrix(path, has_header)
         return ref_core.DataMatrix(d.values, column_names=d.column_names)
 
+    def _conv_path(path):
+        return ref_core.SolutionPath(tuple(
+            ref_core.PathSegment(lambda_lo=sg.lambda_lo, lambda_hi=sg.lambda_hi, line=_conv(sg.line),
+                                 z_lo=sg.z_lo, z_hi=sg.z_hi) for sg in path.segments))
+
+    def merge_path(lambdas, solutions, data):
+        from . import path
+        return _conv_path(path.merge_path(lambdas, solutions, data))
+
+    def solution_path(data, threads=None):
+        from . import path
+        return _conv_path(path.solution_path(data, threads))
+
     targets = {
+        "merge_path": merge_path,
+        "solution_path": solution_path,
         "read_matrix": read_matrix,
         "fit_line": fit_line,
         "fit_for_pivot": fit_for_pivot,
