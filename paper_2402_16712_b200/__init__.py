@@ -18,7 +18,7 @@ _API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspa
 _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions", "merge_path",
          "solution_path")
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
-_IO = ("read_matrix", "write_matrix", "CsvParseError")
+_IO = ("read_matrix", "write_matrix", "CsvParseError", "write_path", "read_path", "write_sweep")
 
 __all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "PathSegment", "SolutionPath", "SubspaceFit", "gen_line_data",
            "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, "__version__"]

@@ -280,6 +280,13 @@ def csv_cases():
                 exp[key] = {"ok": False, "type": "ValueError", "msg": str(e)}
     d, _ = l1line.gen_line_data(7, 5, seed=3, noise_scale=1.0)
     rio.write_matrix(d, os.path.join(out, "written.csv"), header=True)
+    toy = l1line.DataMatrix(np.array([[4.0, -2.0, 3.0, -6.0], [-3.0, 4.0, 2.0, -1.0], [2.0, 3.0, -3.0, -2.0],
+                                      [-3.0, 4.0, 2.0, 3.0], [5.0, 3.0, 2.0, -1.0]]))
+    rio.write_path(l1line.solution_path(toy), os.path.join(out, "toy_path.json"))
+    rio.write_sweep([{"lam": 0.0, "preserved": 3, "error": 34.5, "penalty_norm": 2.5, "objective": 34.5,
+                      "l0_fraction": 0.25, "discordance": None},
+                     {"lam": 1.5, "preserved": 0, "error": 40.1, "penalty_norm": 1.2, "objective": 41.9,
+                      "l0_fraction": 0.5, "discordance": 0.125}], os.path.join(out, "sweep.csv"))
     np.save(os.path.join(out, "written_X.npy"), d.values)
     with open(os.path.join(out, "expected.json"), "w") as f:
         json.dump(exp, f, indent=0, sort_keys=True)
