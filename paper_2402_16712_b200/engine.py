@@ -553,8 +553,15 @@ class DeviceFit:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         piv, cand = ctypes.c_int64(), ctypes.c_int64()
         err, pen, obj = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        hook = _lib.UB_EXCHANGE_FN(0) if ub_exchange is None else \
-            _lib.UB_EXCHANGE_FN(lambda top, ctx: float(ub_exchange(top)))
+        failed = []
+
+        def _exchange(top, ctx):
+            try:
+                return float(ub_exchange(top))
+            except BaseException as e:  # noqa: BLE001 -- re-raised after the C call
+                failed.append(e)
+                return float("nan")  # no threshold: nothing is pruned
+        hook = _lib.UB_EXCHANGE_FN(0) if ub_exchange is None else _lib.UB_EXCHANGE_FN(_exchange)
         if ub_exchange is not None and prune is None:
             prune = self.auto_prune()  # every rank must take the same path
         with torch.cuda.device(self.device):
@@ -563,6 +570,8 @@ class DeviceFit:
                                        -1 if prune is None else int(bool(prune)), hook, None, ctypes.byref(piv),
                                        v.data_ptr(), ctypes.byref(err), ctypes.byref(pen), ctypes.byref(obj),
                                        ctypes.byref(cand), self.ws.data_ptr(), self.ws.numel(), self._s)
+            if failed:
+                raise failed[0]
             if rc == _lib.L1B_EINVAL and math.isinf(lam):
                 raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
             _lib.check(rc, "l1b_fit_line")
