@@ -682,3 +682,17 @@ def test_solution_path_matches_reference():
         assert np.asarray([s.lambda_lo for s in segs]).tobytes() == g[f"{name}_lo"].tobytes(), name
         assert np.asarray([s.line.v for s in segs]).tobytes() == g[f"{name}_v"].tobytes(), name
         assert np.asarray([s.line.objective for s in segs]).tobytes() == g[f"{name}_obj"].tobytes(), name
+
+
+def test_pruned_path_outside_fp32_window():
+    """Magnitudes beyond the FP32 steering window (|x| ~ 2^80, and a column
+    near 2^-70): the bounds prune nothing and every problem goes to the exact
+    straggler solver -- the pruned API path still returns the exact winner."""
+    rng = np.random.default_rng(41)
+    X = rng.standard_normal((600, 40)) * 2.0 ** 80
+    X[:, 3] *= 2.0 ** -150
+    eng = DeviceFit(X)
+    for lam in (0.0, 1e24):
+        want = eng.fit_line_device(lam, prune=False)
+        got = eng.fit_line_device(lam, prune=True)
+        assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes() and got.objective == want.objective
