@@ -369,6 +369,13 @@ def run_ours(args):
         if k >= args.warmup:
             e2e_ms.append(ms)
     lines = list(res.components) if ncomp > 1 else res
+    # optimality certificate of every column of the first winning line (device,
+    # outside the timed region; oracle.py:141-174's dual conditions)
+    cert = None
+    if rank == 0 and ncomp == 1:
+        from paper_2402_16712_b200.certify import certify_line
+        c = certify_line(X, lines[0])
+        cert = {"columns": int(np.isfinite(c.slack).sum()), "refuted": len(c.refuted), "lam": float(lines[0].lam)}
     e2e_val = solves_step * args.steps / (max_over_ranks(float(np.sum(e2e_ms))) / 1e3)
 
     cpu = None
@@ -385,7 +392,7 @@ def run_ours(args):
             "data": "synthetic (reference generator, seed 0)",
             "config": _config_dict(args, X, lams, world),
             "result": {"pivot": [l.preserved for l in lines][:4], "objective": [l.objective for l in lines][:4],
-                       "nonzeros": [int(np.count_nonzero(l.v)) for l in lines][:4]},
+                       "nonzeros": [int(np.count_nonzero(l.v)) for l in lines][:4], "certificate": cert},
             "e2e": {"value": e2e_val, "unit": "solves/s", "ms_per_step": float(np.mean(e2e_ms)),
                     "h2d_bytes_per_step": int(X.nbytes),
                     "d2h_bytes_per_step": int(8 * m * len(lams) * ncomp + 8 * npiv * len(lams) * ncomp)},
