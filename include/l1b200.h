@@ -109,10 +109,12 @@ int l1b_certify_columns(const double* d_X, int64_t n, int64_t m, int64_t pivot, 
  * ONE pass: the histogram range covers the crossings of the smallest and
  * largest penalty (and 0 where the largest may kill the column), and every
  * penalty gets its own bounds from the same histogram and residual.
- * d_lb / d_ub are [nlam][npiv] (device).  The batched lambda sweep (C3). */
+ * d_lb / d_ub are [nlam][npiv] (device).  d_ranges (device, may be NULL):
+ * [nlam][npiv][m] float pairs, each (penalty, pivot, target)'s next range,
+ * for l1b_bound_entries to continue from.  The batched lambda sweep (C3). */
 int l1b_bound_pivots_multi(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam,
-                           int64_t p_begin, int64_t p_stride, int64_t npiv, double* d_lb, double* d_ub, void* d_ws,
-                           size_t ws_bytes, void* stream);
+                           int64_t p_begin, int64_t p_stride, int64_t npiv, double* d_lb, double* d_ub,
+                           void* d_ranges, void* d_ws, size_t ws_bytes, void* stream);
 
 /* l1b_bound_pivots for a pivot list (host memory) with 1 to 3 passes per
  * problem: every further pass re-histograms the range where the previous
@@ -208,12 +210,13 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
  * entries h_pivots[k], h_lams[k] in one launch.  l1b_bound_entries is one
  * bounding pass per entry -- from row samples at the entry's penalty, or,
  * with h_from, continuing from entry h_from[k] of the previous bound call's
- * list of from_count entries; l1b_fit_entries_seeded is the seeded exact fit
+ * list of from_count entries (or, with d_from_ranges, from row h_from[k] of
+ * l1b_bound_pivots_multi's d_ranges); l1b_fit_entries_seeded is the seeded exact fit
  * of entries (h_seed[k]: entry of the last bound call).  Same outputs as the
  * single-penalty calls, per entry. */
 int l1b_bound_entries(const double* d_X, int64_t n, int64_t m, const double* h_lams, const int64_t* h_pivots,
-                      int64_t count, const int64_t* h_from, int64_t from_count, double* d_lb, double* d_ub,
-                      void* d_ws, size_t ws_bytes, void* stream);
+                      int64_t count, const int64_t* h_from, int64_t from_count, const void* d_from_ranges,
+                      double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 int l1b_fit_entries_seeded(const double* d_X, int64_t n, int64_t m, const double* h_lams, const int64_t* h_pivots,
                            int64_t count, const int64_t* h_seed, int64_t seed_count, double* d_V, double* d_err,
                            double* d_pen, double* d_obj, void* d_ws, size_t ws_bytes, void* stream);

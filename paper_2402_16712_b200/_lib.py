@@ -132,14 +132,14 @@ def load() -> ctypes.CDLL:
                                                   _vp, _vp, _sz, _vp]
     lib.l1b_bound_pivots_multi.restype = ctypes.c_int
     lib.l1b_bound_pivots_multi.argtypes = [_vp, _i64, _i64, _vp, ctypes.c_int32, _i64, _i64, _i64, _vp, _vp, _vp,
-                                           _sz, _vp]
+                                           _vp, _sz, _vp]
     lib.l1b_pivot_breakpoints.restype = ctypes.c_int
     lib.l1b_pivot_breakpoints.argtypes = [_vp, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int64), _vp, _vp, _vp, _i64,
                                           _vp, _sz, _vp]
     lib.l1b_certify_columns.restype = ctypes.c_int
     lib.l1b_certify_columns.argtypes = [_vp, _i64, _i64, _i64, _vp, ctypes.c_double, _vp, _vp, _sz, _vp]
     lib.l1b_bound_entries.restype = ctypes.c_int
-    lib.l1b_bound_entries.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_entries.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_fit_entries_seeded.restype = ctypes.c_int
     lib.l1b_fit_entries_seeded.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _sz,
                                            _vp]

@@ -542,15 +542,17 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     H.build();  // once for every penalty
     for (int l = 0; l < P.nlam; ++l) {
       double lb = 0.0, ub = 0.0;
+      float2 nx = make_float2(h ? lo[1] : lo[0], h ? hi[1] : hi[0]);
       if (live) {
         double2 rg;
-        float2 nx;
         column_bounds(H, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
                       (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut,
                       P.lams[l], P.colsum[j], n, sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &rg, &nx);
       } else if (okh && j < m && dgh) {
         lb = ub = P.colsum[j];  // fit.py:66-72: v = 0, error = sum |x|
       }
+      // each penalty's next range, for a continuing pass per (penalty, pivot) entry
+      if (P.NEXTm && okh && j < m) P.NEXTm[((int64_t)l * P.npiv + kh) * m + j] = nx;
       lb = warp_sum(lb);
       ub = warp_sum(ub);
       if (lane == 0 && okh) {

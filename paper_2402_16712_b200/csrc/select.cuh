@@ -88,6 +88,7 @@ struct SelParams {
   const double* lamk;    // per pivot-list entry penalty (entry lists), or null: lam for all
   const double* lams;    // multi-penalty bound: ascending penalties (device)
   int nlam;
+  float2* NEXTm;         // multi-penalty bound: next ranges [nlam][npiv][m] (optional)
   double* LBm;           // multi-penalty bound: per (penalty, pivot) sums [nlam][npiv]
   double* UBm;
 };

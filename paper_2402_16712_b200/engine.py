@@ -271,9 +271,10 @@ class DeviceFit:
             h = out.cpu().numpy()
         return h[0], h[1], h[2]
 
-    def bound_entries(self, lams, pivots, from_pos=None, from_count: int = 0):
+    def bound_entries(self, lams, pivots, from_pos=None, from_count: int = 0, from_ranges=None):
         """One bounding pass per (pivot, penalty) entry (l1b_bound_entries); with
-        from_pos, continuing from those entries of the last bound call."""
+        from_pos, continuing from those entries of the last bound call (or of
+        the multi-penalty pass's ranges, from_ranges)."""
         piv = np.ascontiguousarray(np.asarray(pivots, dtype=np.int64))
         lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
         fp = None if from_pos is None else np.ascontiguousarray(np.asarray(from_pos, dtype=np.int64))
@@ -283,6 +284,7 @@ class DeviceFit:
                 self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                 piv.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), piv.size,
                 None if fp is None else fp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), int(from_count),
+                None if from_ranges is None else from_ranges.data_ptr(),
                 b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._s)
             _lib.check(rc, "l1b_bound_entries")
             bh = b.cpu().numpy()
@@ -305,7 +307,7 @@ class DeviceFit:
         _lib.check(rc, "l1b_fit_entries_seeded")
         return V, eo[0], eo[1], eo[2]
 
-    def _sweep_winners(self, lam, all_piv, lbm, ubm, uniq, ub_exchange):
+    def _sweep_winners(self, lam, all_piv, lbm, ubm, uniq, ub_exchange, ranges=None, npiv: int = 0):
         """Winners of a penalty sweep after one multi-penalty pass: every
         penalty's survivors are refined and fitted together as one entry list
         (one launch per cascade level instead of one per penalty)."""
@@ -337,11 +339,15 @@ class DeviceFit:
             li = np.concatenate([ent_l[i] for i in bl])  # entry -> penalty index
             kk = np.concatenate([ent_k[i] for i in bl])  # entry -> shard pivot position
             seed, seed_n = None, 0
+            src = None
+            if ranges is not None:  # level 0 continues from the multi pass's per-penalty ranges
+                seed, seed_n, src = li * npiv + kk, L * npiv, ranges
             for level in range(REFINE_PASSES + 1):
                 counts = np.bincount(li, minlength=L)
                 if kk.size == 0 or (level > 0 and np.all(counts <= REFINE_MIN)):
                     break
-                lb2, ub2 = self.bound_entries(uniq[li], all_piv[kk], seed, seed_n)
+                lb2, ub2 = self.bound_entries(uniq[li], all_piv[kk], seed, seed_n, src)
+                src = None
                 np.minimum.at(tops, li, ub2)
                 ok = ~(lb2 > np.array([self._prune_threshold(t) for t in tops])[li])
                 sel = np.nonzero(ok)[0]
@@ -360,19 +366,25 @@ class DeviceFit:
                 wins.update(zip(ids, self._winners(groups)))
         return [wins.get(int(np.searchsorted(uniq, x))) for x in lam]
 
-    def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
-        """One bounding pass for several strictly ascending penalties: lb, ub [L][npiv] (host)."""
+    def bound_pivots_multi(self, lams, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None,
+                           ranges: bool = False):
+        """One bounding pass for several strictly ascending penalties: lb, ub [L][npiv]
+        (host); with ranges, also every (penalty, pivot, target)'s next range
+        [L][npiv][m] (device float pairs) for bound_entries to continue from."""
         lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
         if npiv is None:
             npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
         with torch.cuda.device(self.device):
             b = torch.empty((2, lam.size, npiv), dtype=torch.float64, device=self.device)
+            rg = torch.empty((lam.size, npiv, self.m, 2), dtype=torch.float32, device=self.device) if ranges else None
             rc = self.lib.l1b_bound_pivots_multi(
                 self.X.data_ptr(), self.n, self.m, lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), lam.size,
-                p_begin, p_stride, npiv, b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(), self.ws.numel(),
-                self._s)
+                p_begin, p_stride, npiv, b[0].data_ptr(), b[1].data_ptr(), None if rg is None else rg.data_ptr(),
+                self.ws.data_ptr(), self.ws.numel(), self._s)
             _lib.check(rc, "l1b_bound_pivots_multi")
             bh = b.cpu().numpy()
+        if ranges:
+            return bh[0], bh[1], rg
         return bh[0], bh[1]
 
     def bound_pivot_list(self, lam: float, pivots, passes: int = REFINE_PASSES):
@@ -507,8 +519,13 @@ class DeviceFit:
         # is penalty-free; each penalty gets its own bounds from it)
         uniq = np.unique(lam[np.isfinite(lam)])
         if uniq.size > 1 and all(np.isfinite(lam)):
-            lbm, ubm = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv)
-            return self._sweep_winners(lam, all_piv, lbm, ubm, uniq, ub_exchange)
+            # the per-penalty next ranges (8 B per (penalty, pivot, target)) let the
+            # first refinement level continue instead of re-sampling
+            keep_ranges = uniq.size * npiv * self.m * 8 <= (4 << 30)
+            res = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv, ranges=keep_ranges)
+            lbm, ubm = res[0], res[1]
+            rg = res[2] if keep_ranges else None
+            return self._sweep_winners(lam, all_piv, lbm, ubm, uniq, ub_exchange, rg, npiv)
         for l in range(lam.size):
             lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
             fresh = False
