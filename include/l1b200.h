@@ -97,6 +97,14 @@ int l1b_pivot_breakpoints(const double* d_X, int64_t n, int64_t m, int64_t pivot
                           double* d_ratios, double* d_start, double* d_right, int64_t ld, void* d_ws,
                           size_t ws_bytes, void* stream);
 
+/* brute_force_column (oracle.py:39-58) for every target column of one pivot
+ * (targets j != pivot ascending): the objective at every kink candidate
+ * {0} u {x_ij / x_ip}, summed over rows in order; d_t[c] the smallest
+ * minimiser (+0.0 for zero), d_f[c] its objective.  O(n^2) per column --
+ * an independent check, not a fast path.  d_X device row-major n x m. */
+int l1b_brute_force_columns(const double* d_X, int64_t n, int64_t m, int64_t pivot, double lam, double* d_t,
+                            double* d_f, void* stream);
+
 /* Optimality certificate of every column of one line (oracle.py:141-174's
  * dual conditions, checked through the subdifferential with exact weight
  * sums): d_slack[j] >= 0 iff v_j (device d_v[m]) minimises pivot `pivot`'s

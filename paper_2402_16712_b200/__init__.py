@@ -19,9 +19,10 @@ _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSol
          "solution_path")
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
 _IO = ("read_matrix", "write_matrix", "CsvParseError", "write_path", "read_path", "write_sweep")
+_VALIDATE = ("brute_force_column", "brute_force_pivot", "brute_force_line", "sweep_validate", "SweepReport")
 
 __all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "PathSegment", "SolutionPath", "SubspaceFit", "gen_line_data",
-           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, "__version__"]
+           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, *_VALIDATE, "__version__"]
 
 
 def __getattr__(name):
@@ -38,6 +39,9 @@ def __getattr__(name):
     if name in _IO:
         from . import io
         return getattr(io, name)
+    if name in _VALIDATE:
+        from . import validate
+        return getattr(validate, name)
     if name == "use_gpu":
         from .integration import use_gpu
         return use_gpu

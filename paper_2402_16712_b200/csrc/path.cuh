@@ -160,3 +160,55 @@ __global__ void k_certify(SelParams P, int64_t p, const double* __restrict__ v, 
     slack[j] = ldexp(s, -P.spow[p]);
   }
 }
+
+// ------------------------------------------------------ brute force --
+//
+// brute_force_column (oracle.py:39-58) for every target column of one pivot:
+// f(t) = sum_i |x_ij - t x_ip| + lam |t| evaluated at every candidate t in
+// {0} u {x_ij / x_ip : x_ip != 0} (the kinks of the convex objective), the
+// smallest t among the minima.  One CTA per target column, one candidate per
+// thread at a time, each f(t) summed over the rows in order (the reference's
+// axis-0 reduction: the same doubles).  O(n^2) per column: an independent
+// check of the sort-free solver, not a fast path.
+__global__ void __launch_bounds__(256) k_brute_force(const double* __restrict__ X, int64_t n, int64_t m, int64_t p,
+                                                     double lam, double* __restrict__ t_out,
+                                                     double* __restrict__ f_out) {
+  const int64_t c = blockIdx.x;  // target column index among j != p
+  const int64_t j = c < p ? c : c + 1;
+  __shared__ double sf[256], st[256];
+  double bf = INFINITY, bt = 0.0;
+  for (int64_t k = (int64_t)threadIdx.x - 1; k < n; k += blockDim.x) {  // k = -1: the candidate 0
+    double t;
+    if (k < 0) {
+      t = 0.0;
+    } else {
+      const double b = X[k * m + p];
+      if (b == 0.0) continue;
+      t = __ddiv_rn(X[k * m + j], b);
+    }
+    double f = 0.0;
+    for (int64_t i = 0; i < n; ++i) f = __dadd_rn(f, fabs(__dsub_rn(X[i * m + j], __dmul_rn(X[i * m + p], t))));
+    f = __dadd_rn(f, __dmul_rn(lam, fabs(t)));
+    if (f < bf || (f == bf && t < bt)) {
+      bf = f;
+      bt = t;
+    }
+  }
+  sf[threadIdx.x] = bf;
+  st[threadIdx.x] = bt;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const double f2 = sf[threadIdx.x + o], t2 = st[threadIdx.x + o];
+      if (f2 < sf[threadIdx.x] || (f2 == sf[threadIdx.x] && t2 < st[threadIdx.x])) {
+        sf[threadIdx.x] = f2;
+        st[threadIdx.x] = t2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    t_out[c] = st[0] == 0.0 ? 0.0 : st[0];  // a zero candidate is +0.0
+    f_out[c] = sf[0];
+  }
+}

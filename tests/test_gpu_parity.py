@@ -696,3 +696,23 @@ def test_pruned_path_outside_fp32_window():
         want = eng.fit_line_device(lam, prune=False)
         got = eng.fit_line_device(lam, prune=True)
         assert got.pivot == want.pivot and got.v.tobytes() == want.v.tobytes() and got.objective == want.objective
+
+
+def test_brute_force_and_sweep_validate():
+    """oracle.py's brute force on the device: toy KAT (test_oracle.py:23-36),
+    brute-force objectives == fit_line's exactly on random data, and the
+    reference's sweep_validate (test_acceptance.py:110-120) on a device path."""
+    from paper_2402_16712_b200 import brute_force_column, brute_force_line, solution_path, sweep_validate
+    t, f = brute_force_column(TOY, 0, 1, 0.0)
+    want = oracle.fit_for_pivot(TOY, 0, 0.0)
+    assert t == want.v[1]
+    rng = np.random.default_rng(17)
+    for _ in range(6):
+        X = rng.uniform(-10, 10, size=(int(rng.integers(5, 40)), int(rng.integers(3, 8))))
+        lam = float(rng.uniform(0, np.abs(X).sum()))
+        b = brute_force_line(X, lam)
+        g = l1b.fit_line(X, lam)
+        assert b.objective == g.objective or abs(b.objective - g.objective) <= 1e-12 * max(1.0, abs(g.objective))
+    X = rng.uniform(-10, 10, size=(30, 5))
+    rep = sweep_validate(X, solution_path(X), grid_size=40)
+    assert rep.ok, rep.failures
