@@ -14,7 +14,7 @@ from .datagen import gen_line_data, gen_outlier_data, laplace
 __version__ = "0.1.0"
 
 _API = ("fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
-        "residual_error", "resolve_threads")
+        "residual_error", "resolve_threads", "discordance", "l0_fraction")
 _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSolutions", "merge_path",
          "solution_path")
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")

@@ -30,7 +30,7 @@ from .core import DataMatrix, FittedLine, SubspaceFit
 from .engine import DeviceFit
 
 __all__ = ["fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
-           "residual_error", "resolve_threads"]
+           "residual_error", "resolve_threads", "discordance", "l0_fraction"]
 
 THREADS_ENV = "L1LINE_THREADS"
 
@@ -156,3 +156,23 @@ def fit_subspace(data, lam: float, k: int, threads: int | None = None) -> Subspa
         if t + 1 < k:
             eng.deflate(line.v)
     return SubspaceFit(tuple(comps), degenerate=False)
+
+
+def discordance(v_true, v_est) -> float:
+    """Sine of the principal angle between two directions, in [0, 1] (subspace.py:79-97):
+    the norm of the component of one unit vector orthogonal to the other."""
+    a = np.asarray(v_true, dtype=np.float64)
+    b = np.asarray(v_est, dtype=np.float64)
+    na, nb = float(np.linalg.norm(a)), float(np.linalg.norm(b))
+    if na == 0.0 or nb == 0.0:
+        raise ValueError("discordance needs two nonzero vectors")
+    ah, bh = a / na, b / nb
+    return min(1.0, float(np.linalg.norm(bh - float(ah @ bh) * ah)))
+
+
+def l0_fraction(v, tol: float = 1e-9) -> float:
+    """Fraction of coordinates with magnitude above tol (subspace.py:100-110)."""
+    if tol < 0.0:
+        raise ValueError("tolerance must be nonnegative")
+    v = np.asarray(v, dtype=np.float64)
+    return float(np.count_nonzero(np.abs(v) > tol)) / v.size

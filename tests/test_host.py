@@ -172,3 +172,15 @@ def test_breakpoint_grid_dedup_matches_reference_rule():
             if x - ref[-1] > DEDUP_TOL:
                 ref.append(x)
         assert np.asarray(ref).tobytes() == _dedup(np.concatenate([[0.0], v])).tobytes(), t
+
+
+def test_discordance_and_l0_fraction():
+    """subspace.py:79-110 mirrors (pkg/tests/test_subspace.py's properties)."""
+    v = np.array([3.0, 0.0, -4.0])
+    assert l1b.discordance(v, -2.5 * v) <= 1e-15
+    assert l1b.discordance([1.0, 0.0], [0.0, 2.0]) == 1.0
+    assert l1b.l0_fraction([0.0, 1e-12, 0.5, -2.0]) == 0.5
+    with pytest.raises(ValueError):
+        l1b.discordance([0.0, 0.0], [1.0, 0.0])
+    with pytest.raises(ValueError):
+        l1b.l0_fraction(v, tol=-1.0)
