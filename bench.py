@@ -412,13 +412,14 @@ def run_ours(args):
                                        "peak_TOPs": _fp32_peak(dev) / 1e12},
                          "smem_wavefront_view": {
                              "note": "shared-memory pipe cycles the design needs per element: per warp, 4 rows x "
-                                     "2 pivots x 32 targets cost 4 tile + 6 plane loads + 8 atomics = 18 "
+                                     "2 pivots x 64 targets cost 8 tile + 6 plane loads + 16 atomics = 30 "
                                      "wavefronts; peak = one wavefront per SM-clock (the atomic probe / 32). "
-                                     "ncu (profiles/r01/ncu_bound_c2_v13.txt) measures the L1/TEX pipe at 78 %.",
-                             "wavefronts_per_element": 18.0 / 256.0,
-                             "achieved_G_per_s": kb_rate * 18.0 / 256.0 / 1e9,
+                                     "ncu (profiles/r01/ncu_bound_c2_v19.txt) measures the L1/TEX pipe at 74 % and "
+                                     "issue slots at 74 %.",
+                             "wavefronts_per_element": 30.0 / 512.0,
+                             "achieved_G_per_s": kb_rate * 30.0 / 512.0 / 1e9,
                              "peak_G_per_s": atoms_peak / 32.0 / 1e9,
-                             "frac": kb_rate * 18.0 / 256.0 / (atoms_peak / 32.0)},
+                             "frac": kb_rate * 30.0 / 512.0 / (atoms_peak / 32.0)},
                          "step_view": {
                              "note": "whole pruned step against the exact algorithm's FP64 floor (SURVEY.md 8d: "
                                      "11 FP64 ops per ratio element, E = n*m*(m-1) per fit); > 1 means the step "

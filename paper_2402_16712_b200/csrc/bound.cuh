@@ -22,32 +22,32 @@
 // (v_p = 1).  A pivot whose lower bound exceeds the smallest upper bound
 // cannot win; the host fits only the others exactly (l1b_fit_pivot_list).
 //
-// Layout: a CTA is 8 pivots x 32 targets like k_select, but each thread owns
-// TWO problems (pivots 2w, 2w+1 of its warp, same target): one load of the
-// x_ij tile row and one 16-byte load of both pivots' (y, |x_ip|) serve both
-// problems, halving the shared-memory loads per problem, and the two
-// histogram read-modify-write chains interleave.
+// Layout: a CTA is 4 pivots x 64 targets and each thread owns FOUR problems
+// (the 2 pivots of its warp's pair x 2 targets): one x_ij load serves two
+// problems, one 16-byte broadcast of a row pair's (y, x, wq) records serves
+// 128 elements, and the four histogram chains interleave (k_bound below).
 
-constexpr int kBPairs = 4;                 // pivot pairs per k_bound CTA (8 pivots)
-constexpr int kBWarps = 2 * kBPairs;       // two row halves per pair
+constexpr int kBPairs = 2;                 // pivot pairs per k_bound CTA
+constexpr int kBPiv = 2 * kBPairs;         // pivots per CTA (k_group_bound's plane groups)
+constexpr int kBQuarters = 4;              // row quarters per pair
+constexpr int kBWarps = kBPairs * kBQuarters;
 constexpr int kBThreads = kBWarps * 32;
-constexpr int kBSlots = kBPairs * 32;      // histogram columns: (pair, target)
+constexpr int kBSlots = kBPairs * 64;      // histogram columns: (pair, target of 64)
 #ifndef KB_ROWS
 #define KB_ROWS 64
 #endif
 #ifndef KB_STAGES
-#define KB_STAGES 3
-#endif
-#ifndef KB_UNROLL
-#define KB_UNROLL 2
+#define KB_STAGES 2
 #endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
-constexpr int kBTile = kBRows * 32 * 4;    // x_ij float tile [row][32 targets]
-constexpr int kBPlane = kBRows * kWarps * 12;  // k_group_bound records: 12 B per (row, pivot)
-constexpr int kBStage = kBTile + kBPlane;
+constexpr int kBTile = kBRows * 32 * 4;    // one x_ij float tile [row][32 targets]; a stage holds two
+constexpr int kBPlane = kBRows * kBPiv * 12;  // k_group_bound records: 12 B per (row, pivot)
+constexpr int kBStage = 2 * kBTile + kBPlane;
 constexpr int kBStages = KB_STAGES;
-constexpr int kBUnroll = KB_UNROLL;        // 8-row groups per main-loop iteration
-constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [problem][bin][slot], exact 32-bit sums
+constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [pivot of the pair][bin][slot], exact 32-bit sums
+static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
+static_assert(kBRows % (4 * kBQuarters) == 0, "a chunk is whole 4-row groups per quarter");
+static_assert(kBStages * kBStage >= kBQuarters * 4 * kBPairs * 32 * 8, "stage buffers hold the residual shares");
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 // bracket half-width in sample ranks: narrow for the one-pass bound (tight
 // bins), wider when later passes refine it (fewer optima outside)
@@ -353,10 +353,14 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 // range (P.NEXTw), the seed range for the exact solver (P.BRK) and the
 // per-column bounds (P.LB / P.UB).
 //
-// Threads: warps w and w + 4 own the same pivot pair (2w', 2w'+1, w' = w % 4)
-// and target (lane) and split each chunk's rows (alternate 4-row groups);
-// both add into the problem's one histogram with shared-memory atomics, so
-// the CTA holds 8 warps for the histogram space of 4.
+// Threads: a CTA is 4 pivots (2 pairs) x 64 targets (two 32-target tiles of
+// Xft).  Each thread owns FOUR problems: the 2 pivots of its warp's pair x
+// targets (lane, 32 + lane) of the tile pair, so one 16-byte broadcast load
+// of a row pair's plane records serves 2 x 2 x 32 = 128 ratio elements and
+// the shared-memory wavefronts per element drop to 30 / 512 (8 tile loads,
+// 6 record loads, 16 atomics per 4-row group).  The 4 warps of a pair
+// (quarters) split each chunk's rows (4-row groups q, q + 4) and add into the
+// same histograms, so the CTA holds 8 warps for the histogram space of 2.
 // SPLIT (few pivots, many rows: a grid too small to fill the GPU): the rows
 // are also split over blockIdx.z; every CTA adds its histograms into P.GH
 // (exact integer sums, any order), leaves its residual share in P.GE[z] and
@@ -364,48 +368,55 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 template <bool CONT, bool SPLIT, bool MULTI = false>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2][kNB][kBSlots]
+  unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2 pivots of a pair][kNB][kBSlots]
   __shared__ __align__(8) unsigned long long full[kBStages];
   __shared__ unsigned done[kBStages];   // warps finished with the stage's chunk
-  __shared__ float sbr[2][5][kBSlots];  // brackets: problem t's (lo, hi, cen, smin, smax) per slot
-  __shared__ double sec[kBSlots];       // e_j(c) of problem 0 from the other half
+  __shared__ float sbr[2][5][kBSlots];  // brackets: problem (t, slot)'s (lo, hi, cen, smin, smax)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int half = warp / kBPairs, pair = warp % kBPairs, slot = pair * 32 + lane;
+  const int quarter = warp / kBPairs, pair = warp % kBPairs;
+  const int tq = quarter & 1, eq = quarter >> 1;  // the problem this thread prepares and finishes
   const int64_t n = P.n, m = P.m, np = P.np;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  const int64_t tbase = (int64_t)blockIdx.x * np * 32;  // this CTA's target tile
-  const int64_t gbase = (int64_t)blockIdx.y * np * 8;   // this CTA's pivot group
+  const int64_t tile0 = (int64_t)blockIdx.x * 2;  // this CTA's two 32-target tiles of Xft
+  const bool tile1 = (tile0 + 1) * 32 < m;         // the second one exists
+  const int64_t gbase = (int64_t)blockIdx.y * np * kBPiv;  // this CTA's pivot group in the plane
 
-  int64_t kk[2], p[2];
-  bool ok[2], degen[2], act[2];
+  int64_t kk[2], p[2], j[2];
+  bool ok[2], degen[2], act[2][2];
   double Tq[2], unit[2];
+  int slot[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    j[e] = (tile0 + e) * 32 + lane;
+    slot[e] = pair * 64 + e * 32 + lane;
+  }
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    kk[t] = (int64_t)blockIdx.y * kWarps + 2 * pair + t;
+    kk[t] = (int64_t)blockIdx.y * kBPiv + 2 * pair + t;
     ok[t] = kk[t] < P.npiv;
     p[t] = ok[t] ? pivot_of(P, kk[t]) : 0;
     degen[t] = ok[t] && P.nnz[p[t]] == 0;
-    act[t] = ok[t] && !degen[t] && j < m && j != p[t];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) act[t][e] = ok[t] && !degen[t] && j[e] < m && j[e] != p[t];
     Tq[t] = ok[t] && !degen[t] ? P.tq[p[t]] : 0.0;
     unit[t] = ldexp(1.0, ok[t] && !degen[t] ? -P.spow[p[t]] : 0);
   }
-  {  // each half prepares one problem's bracket; both halves need both
-    const bool h = half != 0;
+  {  // each quarter prepares one of the four problems' brackets; all need all
     float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
-    if (h ? act[1] : act[0]) {
+    const int64_t jq = eq ? j[1] : j[0], k = tq ? kk[1] : kk[0];
+    const bool aq = tq ? (eq ? act[1][1] : act[1][0]) : (eq ? act[0][1] : act[0][0]);
+    if (aq) {
       if (CONT) {
-        const int64_t k = h ? kk[1] : kk[0];
-        const float2 r = P.NEXTr[(P.seeds ? P.seeds[k] : k) * m + j];
+        const float2 r = P.NEXTr[(P.seeds ? P.seeds[k] : k) * m + jq];
         b0 = b3 = r.x;
         b1 = b4 = r.y;
         b2 = 0.5f * (r.x + r.y);
       } else {
-        sample_bracket(P, h ? p[1] : p[0], tbase, lane, h ? Tq[1] : Tq[0], h ? unit[1] : unit[0], P.delta, &b0,
-                       &b1, &b2, &b3, &b4, MULTI ? P.lams[0] : lam_of(P, h ? kk[1] : kk[0]),
-                       MULTI ? P.lams[P.nlam - 1] : lam_of(P, h ? kk[1] : kk[0]));
+        sample_bracket(P, tq ? p[1] : p[0], (tile0 + eq) * np * 32, lane, tq ? Tq[1] : Tq[0],
+                       tq ? unit[1] : unit[0], P.delta, &b0, &b1, &b2, &b3, &b4,
+                       MULTI ? P.lams[0] : lam_of(P, k), MULTI ? P.lams[P.nlam - 1] : lam_of(P, k));
       }
     }
-    float* d = &sbr[half][0][slot];
+    float* d = &sbr[tq][0][eq ? slot[1] : slot[0]];
     d[0] = b0;
     d[kBSlots] = b1;
     d[2 * kBSlots] = b2;
@@ -421,9 +432,10 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     const int64_t i0 = (cb + c) * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
     fence_proxy_async();
-    mbar_expect_tx(&full[st], (unsigned)kBStage);
-    bulk_g2s(base, P.Xft + tbase + i0 * 32, kBTile, &full[st]);
-    bulk_g2s(base + kBTile, P.gbp + (gbase + i0 * 8) * 3 / 4, kBPlane, &full[st]);
+    mbar_expect_tx(&full[st], (unsigned)(tile1 ? kBStage : kBStage - kBTile));
+    bulk_g2s(base, P.Xft + tile0 * np * 32 + i0 * 32, kBTile, &full[st]);
+    if (tile1) bulk_g2s(base + kBTile, P.Xft + (tile0 + 1) * np * 32 + i0 * 32, kBTile, &full[st]);
+    bulk_g2s(base + 2 * kBTile, P.gbp + (gbase + i0 * kBPiv) * 3 / 4, kBPlane, &full[st]);
   };
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
@@ -433,79 +445,93 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     mbar_fence_init();
     for (int64_t c = 0; c < min((int64_t)kBStages, nch); ++c) issue(c);
   }
-  // this thread's share of the histograms (problem `half`)
-#pragma unroll
-  for (int b = 0; b < kNB; ++b) hist[(half * kNB + b) * kBSlots + slot] = 0u;
+  for (int x = tid; x < 2 * kNB * kBSlots; x += kBThreads) hist[x] = 0u;
   __syncthreads();
-  float lo[2], hi[2], cf[2], A[2], B[2];
-  unsigned hb[2];
+  float lo[2][2], hi[2][2], cf[2][2], A[2][2], B[2][2];
+  unsigned hb[2][2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    lo[t] = sbr[t][0][slot];
-    hi[t] = sbr[t][1][slot];
-    cf[t] = sbr[t][2][slot];
-    A[t] = (62.f / 63.f) / (hi[t] - lo[t]);
-    B[t] = 0.5f / 63.f - lo[t] * A[t];
-    hb[t] = smem_u32(hist + t * kNB * kBSlots + slot) - 0x4B000000u * (unsigned)(kBSlots * 4);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      lo[t][e] = sbr[t][0][slot[e]];
+      hi[t][e] = sbr[t][1][slot[e]];
+      cf[t][e] = sbr[t][2][slot[e]];
+      A[t][e] = (62.f / 63.f) / (hi[t][e] - lo[t][e]);
+      B[t][e] = 0.5f / 63.f - lo[t][e] * A[t][e];
+      hb[t][e] = smem_u32(hist + t * kNB * kBSlots + slot[e]) - 0x4B000000u * (unsigned)(kBSlots * 4);
+    }
   }
 
   unsigned fphase = 0;
-  const bool busy = __any_sync(0xffffffffu, act[0] || act[1]);
-  double ec0 = 0.0, ec1 = 0.0;  // this half's share of e_j(c) of both problems
+  const bool busy = __any_sync(0xffffffffu, act[0][0] || act[0][1] || act[1][0] || act[1][1]);
+  double ec[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // this quarter's share of e_j(c) of the four problems
   for (int64_t c = 0; c < nch; ++c) {
     const int st = (int)(c % kBStages);
     mbar_wait(&full[st], (fphase >> st) & 1u);
     fphase ^= 1u << st;
     if (busy) {
       const unsigned char* sb = smem + (size_t)st * kBStage;
-      const float* ta = (const float*)sb;
-      // records of this warp's pivot pair: 3 float4 per row pair, 4 pairs per row pair
-      const float4* rec = (const float4*)(sb + kBTile) + pair * 3;
-      float r0acc = 0.f, r1acc = 0.f;
-#pragma unroll kBUnroll
-      for (int r0 = 4 * half; r0 < kBRows; r0 += 8) {
-        float av[4];
-        float4 yw[4];  // (y0, x0, y1, x1) of row r0 + u, as the old plane had it
+      const float* ta = (const float*)sb;  // [2 tiles][kBRows][32]
+      // records of this warp's pivot pair: 3 float4 per row pair and pivot pair
+      const float4* rec = (const float4*)(sb + 2 * kBTile) + pair * 3;
+      float racc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+      for (int r0 = 4 * quarter; r0 < kBRows; r0 += 4 * kBQuarters) {
+        float av[2][4];
+        float4 yw[4];  // (y0, x0, y1, x1) of row r0 + u
         uint2 wu[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) av[u] = ta[(r0 + u) * 32 + lane];
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) av[e][u] = ta[e * kBRows * 32 + (r0 + u) * 32 + lane];
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {  // row pairs (r0, r0+1), (r0+2, r0+3)
-          const float4* rp = rec + ((r0 >> 1) + h2) * 12;
+          const float4* rp = rec + ((r0 >> 1) + h2) * (kBPairs * 3);
           const float4 L0 = rp[0], L1 = rp[1], L2 = rp[2];
           yw[2 * h2] = make_float4(L0.x, L0.z, L0.y, L0.w);
           wu[2 * h2] = make_uint2(__float_as_uint(L1.x), __float_as_uint(L1.y));
           yw[2 * h2 + 1] = make_float4(L1.z, L2.x, L1.w, L2.y);
           wu[2 * h2 + 1] = make_uint2(__float_as_uint(L2.z), __float_as_uint(L2.w));
         }
-        unsigned a0[4], a1[4];
+        // both pivots of the pair at once (packed pairs; same bits as scalar)
+        unsigned a0[2][4], a1[2][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float q0 = av[u] * yw[u].x, q1 = av[u] * yw[u].z;
-          a0[u] = hb[0] + __float_as_uint(fmaf(__saturatef(fmaf(q0, A[0], B[0])), 63.f, 8388608.f)) *
-                              (unsigned)(kBSlots * 4);
-          a1[u] = hb[1] + __float_as_uint(fmaf(__saturatef(fmaf(q1, A[1], B[1])), 63.f, 8388608.f)) *
-                              (unsigned)(kBSlots * 4);
-        }
-        {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 q = fmul2(make_float2(av[e][u], av[e][u]), make_float2(yw[u].x, yw[u].z));
+            const float2 b = ffma2(make_float2(__saturatef(fmaf(q.x, A[0][e], B[0][e])),
+                                               __saturatef(fmaf(q.y, A[1][e], B[1][e]))),
+                                   make_float2(63.f, 63.f), make_float2(8388608.f, 8388608.f));
+            a0[e][u] = hb[0][e] + __float_as_uint(b.x) * (unsigned)(kBSlots * 4);
+            a1[e][u] = hb[1][e] + __float_as_uint(b.y) * (unsigned)(kBSlots * 4);
+          }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
           float e0[4], e1[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            e0[u] = fabsf(fmaf(-cf[0], yw[u].y, av[u]));
-            e1[u] = fabsf(fmaf(-cf[1], yw[u].w, av[u]));
+            const float2 r = ffma2(make_float2(-cf[0][e], -cf[1][e]), make_float2(yw[u].y, yw[u].w),
+                                   make_float2(av[e][u], av[e][u]));
+            e0[u] = fabsf(r.x);
+            e1[u] = fabsf(r.y);
           }
-          r0acc += (e0[0] + e0[1]) + (e0[2] + e0[3]);
-          r1acc += (e1[0] + e1[1]) + (e1[2] + e1[3]);
+          racc[0][e] += (e0[0] + e0[1]) + (e0[2] + e0[3]);
+          racc[1][e] += (e1[0] + e1[1]) + (e1[2] + e1[3]);
         }
-        // fire-and-forget shared adds (the other half adds into the same bins)
+        // fire-and-forget shared adds (the other quarters add into the same bins)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[u]), "r"(wu[u].x));
-          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[u]), "r"(wu[u].y));
-        }
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[e][u]), "r"(wu[u].x));
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[e][u]), "r"(wu[u].y));
+          }
       }
-      ec0 += (double)r0acc;
-      ec1 += (double)r1acc;
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) ec[t][e] += (double)racc[t][e];
     }
     __syncwarp();
     if (lane == 0) {
@@ -521,51 +547,57 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
       }
     }
   }
-  // half 1 finishes problem 1 with half 0's share of its residual, half 0
-  // problem 0 with half 1's share
-  if (half == 1) sec[slot] = ec0;
-  __syncthreads();  // also: both halves' histogram adds are in
-  const double ec = half == 0 ? ec0 + sec[slot] : 0.0;
+  // every chunk has been waited for, so no bulk copy is in flight: the stage
+  // buffers carry the quarters' residual shares to the problem's finisher
+  __syncthreads();  // also: every quarter's histogram adds are in
+  double* ecx = (double*)smem;  // [quarter][t][e][pair][lane]
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) ecx[((quarter * 2 + t) * 2 + e) * (kBPairs * 32) + pair * 32 + lane] = ec[t][e];
   __syncthreads();
-  if (half == 0) sec[slot] = ec1;
-  __syncthreads();
-  const bool h = half != 0;
-  const double ect = h ? ec1 + sec[slot] : ec;
+  double ect = 0.0;
+#pragma unroll
+  for (int q = 0; q < kBQuarters; ++q) ect += ecx[((q * 2 + tq) * 2 + eq) * (kBPairs * 32) + pair * 32 + lane];
+  // this thread's problem (tq, eq), picked with selects (no local-memory arrays)
+  auto pk2 = [&](auto (&a)[2][2]) { return tq ? (eq ? a[1][1] : a[1][0]) : (eq ? a[0][1] : a[0][0]); };
+  const int64_t jj = eq ? j[1] : j[0];
+  const int sl = eq ? slot[1] : slot[0];
+  const float tlo = pk2(lo), thi = pk2(hi), tcf = pk2(cf);
+  const int64_t kq = tq ? kk[1] : kk[0], pq = tq ? p[1] : p[0];
+  const bool okq = tq ? ok[1] : ok[0], dgq = tq ? degen[1] : degen[0];
+  const double Tqq = tq ? Tq[1] : Tq[0], utq = tq ? unit[1] : unit[0];
   if (MULTI) {
     // every penalty in P.lams (ascending): the column bounds summed over the
     // warp's 32 targets (one pivot), one atomic per warp and penalty
-    const bool okh = h ? ok[1] : ok[0], dgh = h ? degen[1] : degen[0];
-    const bool live = okh && j < m && !dgh && j != (h ? p[1] : p[0]);
-    const double ut = h ? unit[1] : unit[0];
-    const int64_t kh = h ? kk[1] : kk[0];
-    Prefix H{hist + half * kNB * kBSlots + slot, kBSlots};
+    const bool live = okq && jj < m && !dgq && jj != pq;
+    Prefix H{hist + tq * kNB * kBSlots + sl, kBSlots};
     H.build();  // once for every penalty
     for (int l = 0; l < P.nlam; ++l) {
       double lb = 0.0, ub = 0.0;
-      float2 nx = make_float2(h ? lo[1] : lo[0], h ? hi[1] : hi[0]);
+      float2 nx = make_float2(tlo, thi);
       if (live) {
         double2 rg;
-        column_bounds(H, ldexp(ut, 21), (double)(h ? lo[1] : lo[0]),
-                      (double)(h ? hi[1] : hi[0]), (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut,
-                      P.lams[l], P.colsum[j], n, sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &rg, &nx);
-      } else if (okh && j < m && dgh) {
-        lb = ub = P.colsum[j];  // fit.py:66-72: v = 0, error = sum |x|
+        column_bounds(H, ldexp(utq, 21), (double)tlo, (double)thi, (double)tcf, ect, Tqq * utq,
+                      P.lams[l], P.colsum[jj], n, sbr[tq][3][sl], sbr[tq][4][sl], &lb, &ub, &rg, &nx);
+      } else if (okq && jj < m && dgq) {
+        lb = ub = P.colsum[jj];  // fit.py:66-72: v = 0, error = sum |x|
       }
       // each penalty's next range, for a continuing pass per (penalty, pivot) entry
-      if (P.NEXTm && okh && j < m) P.NEXTm[((int64_t)l * P.npiv + kh) * m + j] = nx;
+      if (P.NEXTm && okq && jj < m) P.NEXTm[((int64_t)l * P.npiv + kq) * m + jj] = nx;
       lb = warp_sum(lb);
       ub = warp_sum(ub);
-      if (lane == 0 && okh) {
-        atomicAdd(&P.LBm[l * P.npiv + kh], lb);
-        atomicAdd(&P.UBm[l * P.npiv + kh], ub);
+      if (lane == 0 && okq) {
+        atomicAdd(&P.LBm[l * P.npiv + kq], lb);
+        atomicAdd(&P.UBm[l * P.npiv + kq], ub);
       }
     }
     return;
   }
-  if (j >= m || !(h ? ok[1] : ok[0])) return;
-  const int64_t o = (h ? kk[1] : kk[0]) * m + j;
+  if (jj >= m || !okq) return;
+  const int64_t o = kq * m + jj;
   if (SPLIT) {
-    const unsigned* hc = hist + half * kNB * kBSlots + slot;
+    const unsigned* hc = hist + tq * kNB * kBSlots + sl;
     for (int b = 0; b < kNB; ++b) {
       const unsigned x = hc[b * kBSlots];
       if (x) atomicAdd(&P.GH[o * kNB + b], x);
@@ -573,31 +605,27 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     P.GE[(int64_t)blockIdx.z * P.npiv * m + o] = ect;
     if (blockIdx.z == 0) {
       float* g = P.GB + o * 5;
-      g[0] = h ? lo[1] : lo[0];
-      g[1] = h ? hi[1] : hi[0];
-      g[2] = h ? cf[1] : cf[0];
-      g[3] = sbr[half][3][slot];
-      g[4] = sbr[half][4][slot];
+      g[0] = tlo;
+      g[1] = thi;
+      g[2] = tcf;
+      g[3] = sbr[tq][3][sl];
+      g[4] = sbr[tq][4][sl];
     }
     return;
   }
-  const bool dg = h ? degen[1] : degen[0];
-  const float tlo = h ? lo[1] : lo[0], thi = h ? hi[1] : hi[0];
-  if (dg || j == (h ? p[1] : p[0])) {
-    const double z = dg ? P.colsum[j] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
+  if (dgq || jj == pq) {
+    const double z = dgq ? P.colsum[jj] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
     P.LB[o] = z;
     P.UB[o] = z;
     P.BRK[o] = make_double2(-INFINITY, INFINITY);
     P.NEXTw[o] = make_float2(tlo, thi);
     return;
   }
-  const double ut = h ? unit[1] : unit[0];
   double lb, ub;
-  Prefix H{hist + half * kNB * kBSlots + slot, kBSlots};
+  Prefix H{hist + tq * kNB * kBSlots + sl, kBSlots};
   H.build();
-  column_bounds(H, ldexp(ut, 21), (double)tlo, (double)thi,
-                (double)(h ? cf[1] : cf[0]), ect, (h ? Tq[1] : Tq[0]) * ut, lam_of(P, h ? kk[1] : kk[0]), P.colsum[j], n,
-                sbr[half][3][slot], sbr[half][4][slot], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
+  column_bounds(H, ldexp(utq, 21), (double)tlo, (double)thi, (double)tcf, ect, Tqq * utq,
+                lam_of(P, kq), P.colsum[jj], n, sbr[tq][3][sl], sbr[tq][4][sl], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
   P.LB[o] = lb;
   P.UB[o] = ub;
 }
