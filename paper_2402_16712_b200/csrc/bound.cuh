@@ -36,6 +36,9 @@ constexpr int kBSlots = kBPairs * 64;      // histogram columns: (pair, target o
 #ifndef KB_ROWS
 #define KB_ROWS 64
 #endif
+#ifndef KB_GUNROLL
+#define KB_GUNROLL 4  // 4-row groups of a chunk unrolled per warp (a 64-row chunk has 4)
+#endif
 #ifndef KB_STAGES
 #define KB_STAGES 2
 #endif
@@ -44,6 +47,7 @@ constexpr int kBTile = kBRows * 32 * 4;    // one x_ij float tile [row][32 targe
 constexpr int kBPlane = kBRows * kBPiv * 12;  // k_group_bound records: 12 B per (row, pivot)
 constexpr int kBStage = 2 * kBTile + kBPlane;
 constexpr int kBStages = KB_STAGES;
+constexpr int kBGUnroll = KB_GUNROLL;
 constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [pivot of the pair][bin][slot], exact 32-bit sums
 static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
 static_assert(kBRows % (4 * kBQuarters) == 0, "a chunk is whole 4-row groups per quarter");
@@ -380,43 +384,54 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   const bool tile1 = (tile0 + 1) * 32 < m;         // the second one exists
   const int64_t gbase = (int64_t)blockIdx.y * np * kBPiv;  // this CTA's pivot group in the plane
 
-  int64_t kk[2], p[2], j[2];
-  bool ok[2], degen[2], act[2][2];
-  double Tq[2], unit[2];
-  int slot[2];
+  // this thread's own problem (tq, eq): bracketed before the main loop and
+  // finished after it; its metadata is recomputed there instead of living
+  // in registers through the loop
+  const int64_t jq = (tile0 + eq) * 32 + lane;
+  const int slq = pair * 64 + eq * 32 + lane;
+  auto meta = [&](int64_t& k, int64_t& pv, bool& okk, bool& dg, double& T, double& u) {
+    k = (int64_t)blockIdx.y * kBPiv + 2 * pair + tq;
+    okk = k < P.npiv;
+    pv = okk ? pivot_of(P, k) : 0;
+    dg = okk && P.nnz[pv] == 0;
+    T = okk && !dg ? P.tq[pv] : 0.0;
+    u = ldexp(1.0, okk && !dg ? -P.spow[pv] : 0);
+  };
+  bool busy;  // the warp has a live problem
+  {
+    bool any = false;
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    j[e] = (tile0 + e) * 32 + lane;
-    slot[e] = pair * 64 + e * 32 + lane;
-  }
+    for (int t = 0; t < 2; ++t) {
+      const int64_t k = (int64_t)blockIdx.y * kBPiv + 2 * pair + t;
+      const bool okk = k < P.npiv;
+      const int64_t pv = okk ? pivot_of(P, k) : 0;
+      const bool dg = okk && P.nnz[pv] == 0;
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    kk[t] = (int64_t)blockIdx.y * kBPiv + 2 * pair + t;
-    ok[t] = kk[t] < P.npiv;
-    p[t] = ok[t] ? pivot_of(P, kk[t]) : 0;
-    degen[t] = ok[t] && P.nnz[p[t]] == 0;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) act[t][e] = ok[t] && !degen[t] && j[e] < m && j[e] != p[t];
-    Tq[t] = ok[t] && !degen[t] ? P.tq[p[t]] : 0.0;
-    unit[t] = ldexp(1.0, ok[t] && !degen[t] ? -P.spow[p[t]] : 0);
+      for (int e = 0; e < 2; ++e) {
+        const int64_t jj = (tile0 + e) * 32 + lane;
+        any |= okk && !dg && jj < m && jj != pv;
+      }
+    }
+    busy = __any_sync(0xffffffffu, any);
   }
   {  // each quarter prepares one of the four problems' brackets; all need all
     float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
-    const int64_t jq = eq ? j[1] : j[0], k = tq ? kk[1] : kk[0];
-    const bool aq = tq ? (eq ? act[1][1] : act[1][0]) : (eq ? act[0][1] : act[0][0]);
-    if (aq) {
+    int64_t k, pv;
+    bool okk, dg;
+    double T, u;
+    meta(k, pv, okk, dg, T, u);
+    if (okk && !dg && jq < m && jq != pv) {
       if (CONT) {
         const float2 r = P.NEXTr[(P.seeds ? P.seeds[k] : k) * m + jq];
         b0 = b3 = r.x;
         b1 = b4 = r.y;
         b2 = 0.5f * (r.x + r.y);
       } else {
-        sample_bracket(P, tq ? p[1] : p[0], (tile0 + eq) * np * 32, lane, tq ? Tq[1] : Tq[0],
-                       tq ? unit[1] : unit[0], P.delta, &b0, &b1, &b2, &b3, &b4,
+        sample_bracket(P, pv, (tile0 + eq) * np * 32, lane, T, u, P.delta, &b0, &b1, &b2, &b3, &b4,
                        MULTI ? P.lams[0] : lam_of(P, k), MULTI ? P.lams[P.nlam - 1] : lam_of(P, k));
       }
     }
-    float* d = &sbr[tq][0][eq ? slot[1] : slot[0]];
+    float* d = &sbr[tq][0][slq];
     d[0] = b0;
     d[kBSlots] = b1;
     d[2 * kBSlots] = b2;
@@ -447,23 +462,22 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   }
   for (int x = tid; x < 2 * kNB * kBSlots; x += kBThreads) hist[x] = 0u;
   __syncthreads();
-  float lo[2][2], hi[2][2], cf[2][2], A[2][2], B[2][2];
+  float cf[2][2], A[2][2], B[2][2];
   unsigned hb[2][2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      lo[t][e] = sbr[t][0][slot[e]];
-      hi[t][e] = sbr[t][1][slot[e]];
-      cf[t][e] = sbr[t][2][slot[e]];
-      A[t][e] = (62.f / 63.f) / (hi[t][e] - lo[t][e]);
-      B[t][e] = 0.5f / 63.f - lo[t][e] * A[t][e];
-      hb[t][e] = smem_u32(hist + t * kNB * kBSlots + slot[e]) - 0x4B000000u * (unsigned)(kBSlots * 4);
+      const int sl = pair * 64 + e * 32 + lane;
+      const float l = sbr[t][0][sl], h = sbr[t][1][sl];
+      cf[t][e] = sbr[t][2][sl];
+      A[t][e] = (62.f / 63.f) / (h - l);
+      B[t][e] = 0.5f / 63.f - l * A[t][e];
+      hb[t][e] = smem_u32(hist + t * kNB * kBSlots + sl) - 0x4B000000u * (unsigned)(kBSlots * 4);
     }
   }
 
   unsigned fphase = 0;
-  const bool busy = __any_sync(0xffffffffu, act[0][0] || act[0][1] || act[1][0] || act[1][1]);
   double ec[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // this quarter's share of e_j(c) of the four problems
   for (int64_t c = 0; c < nch; ++c) {
     const int st = (int)(c % kBStages);
@@ -475,7 +489,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
       // records of this warp's pivot pair: 3 float4 per row pair and pivot pair
       const float4* rec = (const float4*)(sb + 2 * kBTile) + pair * 3;
       float racc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll
+#pragma unroll kBGUnroll
       for (int r0 = 4 * quarter; r0 < kBRows; r0 += 4 * kBQuarters) {
         float av[2][4];
         float4 yw[4];  // (y0, x0, y1, x1) of row r0 + u
@@ -559,14 +573,13 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   double ect = 0.0;
 #pragma unroll
   for (int q = 0; q < kBQuarters; ++q) ect += ecx[((q * 2 + tq) * 2 + eq) * (kBPairs * 32) + pair * 32 + lane];
-  // this thread's problem (tq, eq), picked with selects (no local-memory arrays)
-  auto pk2 = [&](auto (&a)[2][2]) { return tq ? (eq ? a[1][1] : a[1][0]) : (eq ? a[0][1] : a[0][0]); };
-  const int64_t jj = eq ? j[1] : j[0];
-  const int sl = eq ? slot[1] : slot[0];
-  const float tlo = pk2(lo), thi = pk2(hi), tcf = pk2(cf);
-  const int64_t kq = tq ? kk[1] : kk[0], pq = tq ? p[1] : p[0];
-  const bool okq = tq ? ok[1] : ok[0], dgq = tq ? degen[1] : degen[0];
-  const double Tqq = tq ? Tq[1] : Tq[0], utq = tq ? unit[1] : unit[0];
+  const int64_t jj = jq;
+  const int sl = slq;
+  const float tlo = sbr[tq][0][sl], thi = sbr[tq][1][sl], tcf = sbr[tq][2][sl];
+  int64_t kq, pq;
+  bool okq, dgq;
+  double Tqq, utq;
+  meta(kq, pq, okq, dgq, Tqq, utq);
   if (MULTI) {
     // every penalty in P.lams (ascending): the column bounds summed over the
     // warp's 32 targets (one pivot), one atomic per warp and penalty
