@@ -361,8 +361,8 @@ class DeviceFit:
                     e = np.nonzero(li == i)[0]
                     if e.size:
                         ids.append(i)
-                        groups.append((float(uniq[i]), all_piv[kk[e]], V[torch.as_tensor(e, device=V.device)],
-                                       obj_h[e]))
+                        # rows e of V, gathered only for the re-scored candidates (one gather for all)
+                        groups.append((float(uniq[i]), all_piv[kk[e]], (V, e), obj_h[e]))
                 wins.update(zip(ids, self._winners(groups)))
         return [wins.get(int(np.searchsorted(uniq, x))) for x in lam]
 
@@ -455,12 +455,22 @@ class DeviceFit:
                 raise ValueError(f"objective nan for lam={lam!r} (zero pivot column at infinite penalty)")
             picks.append(self._candidates(obj_h))
         pivs = np.concatenate([np.asarray(g[1])[c] for g, c in zip(groups, picks)]).astype(np.int64)
+        # a group's V is a [k][m] tensor or (V, e): rows e of a shared [K][m] tensor
+        lazy = all(isinstance(g[2], tuple) for g in groups) and len({id(g[2][0]) for g in groups}) == 1
         if pivs.size == 1:  # the common case: one candidate, no batching copies
-            row = groups[0][2][int(picks[0][0])]
+            V = groups[0][2]
+            row = V[0][int(V[1][picks[0][0]])] if isinstance(V, tuple) else V[int(picks[0][0])]
             errs = [self.residual_exact(row, int(pivs[0]))]
             vhs = row.cpu().numpy()[None, :]
         else:
-            rows = torch.cat([V[torch.as_tensor(c, device=V.device)] for (_, _, V, _), c in zip(groups, picks)])
+            if lazy:
+                Vb = groups[0][2][0]
+                idx = np.concatenate([g[2][1][c] for g, c in zip(groups, picks)]).astype(np.int64)
+                rows = Vb[torch.from_numpy(idx).to(Vb.device)]
+            else:
+                rows = torch.cat([(V[0][torch.as_tensor(V[1], device=V[0].device)] if isinstance(V, tuple) else V)
+                                  [torch.as_tensor(c, device=(V[0] if isinstance(V, tuple) else V).device)]
+                                  for (_, _, V, _), c in zip(groups, picks)])
             errs = self.residual_exact_batch(rows, pivs)
             vhs = rows.cpu().numpy()
         out, at = [], 0
