@@ -58,7 +58,10 @@ constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 #ifndef KB_DELTA1
 #define KB_DELTA1 8
 #endif
-constexpr int kBDelta1 = KB_DELTA1, kBDeltaN = 10;
+#ifndef KB_DELTAN
+#define KB_DELTAN 10
+#endif
+constexpr int kBDelta1 = KB_DELTA1, kBDeltaN = KB_DELTAN;
 
 // Bounds of one column optimum from its histogram h[slot * hs] (exact sums
 // of 32-bit weights of q each) over the bracket [lo, hi) (62 interior bins),
