@@ -266,15 +266,18 @@ __device__ __forceinline__ float key2f(unsigned k) {
 
 // lam_lo < lam_hi (one pass for several penalties): the bracket covers the
 // estimated crossings of both, and 0 when lam_hi may kill the column.
-__device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
-                                               double unit, int delta, float* lo, float* hi, float* cen,
-                                               float* smin, float* smax, double lam_lo, double lam_hi) {
+// rep / nrep: the sample is rows (s * nrep + rep) of a stratified 32 * nrep
+// row grid (nrep = 1: rows (2s + 1) n / 64).
+__device__ __forceinline__ void sample_bracket1(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
+                                                double unit, int delta, float* lo, float* hi, float* cen,
+                                                float* smin, float* smax, double lam_lo, double lam_hi, int rep,
+                                                int nrep) {
   const int64_t n = P.n;
   float sr[kSample], sw[kSample];
   float wmax = 0.f;
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
-    const int64_t r = ((2 * s + 1) * n) / (2 * kSample);
+    const int64_t r = ((2 * ((int64_t)s * nrep + rep) + 1) * n) / (2 * (int64_t)kSample * nrep);
     const float2 f = P.pf[p * P.np + r];
     sr[s] = P.Xft[tbase + r * 32 + lane] * f.x;
     sw[s] = fabsf(f.y);
@@ -350,6 +353,68 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
   *smax = key2f((key[kSample - 1] & 0xffffff00u) | 0xffu);
 }
 
+// Tall columns: nrep independent 32-row samples (interleaved strata); their
+// crossing estimates are averaged and the bracket half-widths shrink by
+// sqrt(nrep), the same coverage around an estimate sqrt(nrep) times tighter,
+// so the histogram's bins (and the bounds' slack) narrow with it.  Short
+// columns (the sample stage would cost a visible share of the pass) keep one.
+#ifndef KB_SREP_ROWS
+#define KB_SREP_ROWS 8192  // rows per extra sample
+#endif
+#ifndef KB_SREP_MAX
+#define KB_SREP_MAX 16
+#endif
+__device__ __forceinline__ void sample_bracket_reps(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
+                                                 double unit, int delta, float* lo, float* hi, float* cen,
+                                                 float* smin, float* smax, double lam_lo, double lam_hi, int nrep) {
+  float sc = 0.f, sl = 0.f, sh = 0.f, mn = INFINITY, mx = -INFINITY;
+  bool zero = false;
+#pragma unroll 1
+  for (int rep = 0; rep < nrep; ++rep) {
+    float l, h, c, a, b;
+    sample_bracket1(P, p, tbase, lane, Tq, unit, delta, &l, &h, &c, &a, &b, lam_lo, lam_hi, rep, nrep);
+    zero |= lam_hi > lam_lo && l <= 0.f && h >= 0.f;
+    sc += c;
+    sl += c - l;
+    sh += h - c;
+    mn = fminf(mn, a);
+    mx = fmaxf(mx, b);
+  }
+  const float inv = 1.f / (float)nrep, shrink = rsqrtf((float)nrep);
+  const float c = sc * inv;
+  float l = c - sl * inv * shrink, h = c + sh * inv * shrink;
+  if (!(h > l)) {
+    const float e = fmaxf(fabsf(c), 1e-30f) * 1e-3f;
+    l = c - e;
+    h = c + e;
+  }
+  if (zero) {  // some sample saw the column possibly dead at lam_hi
+    l = fminf(l, 0.f);
+    h = fmaxf(h, 0.f);
+  }
+  *lo = l;
+  *hi = h;
+  *cen = fminf(fmaxf(c, l), h);
+  *smin = mn;
+  *smax = mx;
+}
+// TALL (a k_bound template flag, so short columns' kernels never carry the
+// accumulators): nrep = n / KB_SREP_ROWS samples, at most KB_SREP_MAX.
+__host__ __device__ __forceinline__ int sample_reps(int64_t n) {
+  const int64_t q = n / KB_SREP_ROWS;
+  return q < 1 ? 1 : (q > KB_SREP_MAX ? KB_SREP_MAX : (int)q);
+}
+template <bool TALL>
+__device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
+                                               double unit, int delta, float* lo, float* hi, float* cen,
+                                               float* smin, float* smax, double lam_lo, double lam_hi) {
+  if (TALL)
+    sample_bracket_reps(P, p, tbase, lane, Tq, unit, delta, lo, hi, cen, smin, smax, lam_lo, lam_hi,
+                        sample_reps(P.n));
+  else
+    sample_bracket1(P, p, tbase, lane, Tq, unit, delta, lo, hi, cen, smin, smax, lam_lo, lam_hi, 0, 1);
+}
+
 // One bounding pass per (pivot, target) problem.  CONT = false: the range
 // comes from a row sample (sample_bracket, half-width P.delta ranks).
 // CONT = true (refinement for the pivots an earlier pass could not rule out):
@@ -372,7 +437,7 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 // are also split over blockIdx.z; every CTA adds its histograms into P.GH
 // (exact integer sums, any order), leaves its residual share in P.GE[z] and
 // (z = 0) the ranges in P.GB, and k_bound_epi finishes each problem.
-template <bool CONT, bool SPLIT, bool MULTI = false>
+template <bool CONT, bool SPLIT, bool MULTI = false, bool TALL = false>
 __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2 pivots of a pair][kNB][kBSlots]
@@ -430,7 +495,7 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
         b1 = b4 = r.y;
         b2 = 0.5f * (r.x + r.y);
       } else {
-        sample_bracket(P, pv, (tile0 + eq) * np * 32, lane, T, u, P.delta, &b0, &b1, &b2, &b3, &b4,
+        sample_bracket<TALL>(P, pv, (tile0 + eq) * np * 32, lane, T, u, P.delta, &b0, &b1, &b2, &b3, &b4,
                        MULTI ? P.lams[0] : lam_of(P, k), MULTI ? P.lams[P.nlam - 1] : lam_of(P, k));
       }
     }

@@ -410,6 +410,24 @@ def test_pruned_fit_equals_full_fit():
             assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
 
 
+def test_pruned_fit_equals_full_fit_tall():
+    """Tall columns (n >= 2 * KB_SREP_ROWS) start the bound pass from several
+    averaged row samples (k_bound<..., TALL>); single- and multi-penalty pruned
+    fits, also on deflated data, still return exactly the full fit."""
+    d, _ = l1b.gen_line_data(24, 40000, seed=5, noise_scale=1.0)
+    X = d.values
+    T = float(np.abs(X).sum(axis=0).max())
+    eng = DeviceFit(X)
+    for comp in range(2):
+        for lams in ([1.0], [0.05 * T], [0.0, 1.0, 0.1 * T, 0.5 * T, math.inf]):
+            full = eng.shard_winners(lams, prune=False)
+            pruned = eng.shard_winners(lams, prune=True)
+            for a, b in zip(full, pruned):
+                assert a.pivot == b.pivot and a.v.tobytes() == b.v.tobytes()
+                assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
+        eng.deflate(full[0].v)
+
+
 @pytest.mark.parametrize("m,n", [(300, 2000), (40, 70000)])
 def test_seeded_exact_fit_equals_batched_fit(m, n):
     """l1b_fit_pivot_list_seeded (warp-per-problem solver started on the bound
