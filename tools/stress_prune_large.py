@@ -3,15 +3,18 @@ returns exactly the unpruned winner: random shapes, Gaussian / Cauchy / tied /
 sparse / line / badly scaled / grid data, four penalties each.
 
     python tools/stress_prune_large.py SEED SECONDS  (m 150-500, n 500-20000)
+    STRESS_M=20-80 STRESS_N=16384-120000 python tools/stress_prune_large.py ...  (tall columns)
 """
 import sys, os, time, numpy as np, torch
 sys.path.insert(0, os.getcwd())
 import paper_2402_16712_b200 as l1b
 from paper_2402_16712_b200.engine import DeviceFit
+M_LO, M_HI = map(int, os.environ.get("STRESS_M", "150-500").split("-"))
+N_LO, N_HI = map(int, os.environ.get("STRESS_N", "500-20000").split("-"))
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 bad = 0; t0 = time.time(); cnt = 0
 while time.time() - t0 < float(sys.argv[2]) if len(sys.argv) > 2 else 60:
-    m = int(rng.integers(150, 500)); n = int(rng.integers(500, 20000))
+    m = int(rng.integers(M_LO, M_HI)); n = int(rng.integers(N_LO, N_HI))
     kind = int(rng.integers(0, 7))
     if kind == 0:
         X = rng.standard_normal((n, m))
