@@ -359,10 +359,10 @@ __device__ __forceinline__ void sample_bracket1(const SelParams& P, int64_t p, i
 // so the histogram's bins (and the bounds' slack) narrow with it.  Short
 // columns (the sample stage would cost a visible share of the pass) keep one.
 #ifndef KB_SREP_ROWS
-#define KB_SREP_ROWS 8192  // rows per extra sample
+#define KB_SREP_ROWS 4096  // rows per extra sample
 #endif
 #ifndef KB_SREP_MAX
-#define KB_SREP_MAX 16
+#define KB_SREP_MAX 12
 #endif
 __device__ __forceinline__ void sample_bracket_reps(const SelParams& P, int64_t p, int64_t tbase, int lane, double Tq,
                                                  double unit, int delta, float* lo, float* hi, float* cen,

@@ -411,7 +411,7 @@ def test_pruned_fit_equals_full_fit():
 
 
 def test_pruned_fit_equals_full_fit_tall():
-    """Tall columns (n >= 2 * KB_SREP_ROWS) start the bound pass from several
+    """Tall columns (n >= 2 * KB_SREP_ROWS = 8192) start the bound pass from several
     averaged row samples (k_bound<..., TALL>); single- and multi-penalty pruned
     fits, also on deflated data, still return exactly the full fit."""
     d, _ = l1b.gen_line_data(24, 40000, seed=5, noise_scale=1.0)
