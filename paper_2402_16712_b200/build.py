@@ -34,7 +34,7 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, s) for s in os.listdir(CSRC) if s.endswith((".cu", ".cuh", ".h"))]
+    deps = [os.path.join(CSRC, s) for s in os.listdir(CSRC) if s.endswith((".cu", ".cuh", ".h", ".inc"))]
     deps.append(os.path.join(_HERE, "..", "include", "l1b200.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 

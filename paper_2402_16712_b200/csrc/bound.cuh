@@ -22,36 +22,48 @@
 // (v_p = 1).  A pivot whose lower bound exceeds the smallest upper bound
 // cannot win; the host fits only the others exactly (l1b_fit_pivot_list).
 //
-// Layout: a CTA is 4 pivots x 64 targets and each thread owns FOUR problems
-// (the 2 pivots of its warp's pair x 2 targets): one x_ij load serves two
-// problems, one 16-byte broadcast of a row pair's (y, x, wq) records serves
-// 128 elements, and the four histogram chains interleave (k_bound below).
+// Layout: a CTA is 4 pivots x 128 targets (512 problems) in 16 warps.  A
+// thread owns EIGHT problems, the four pivots x two targets (lane + 32 e) of
+// its warp's half of the tile; the 8 warps of a half split the rows.  Per
+// row a thread loads two x_ij and the four pivots' (y | x | w) records (three
+// broadcast 16-byte loads) and does 8 ratio elements, so the shared-memory
+// pipe carries 16 atomics + 4 tile + 12 record wavefronts per 512 elements
+// (k_bound below).
 
-constexpr int kBPairs = 2;                 // pivot pairs per k_bound CTA
-constexpr int kBPiv = 2 * kBPairs;         // pivots per CTA (k_group_bound's plane groups)
-constexpr int kBQuarters = 4;              // row quarters per pair
-constexpr int kBWarps = kBPairs * kBQuarters;
-constexpr int kBThreads = kBWarps * 32;
-constexpr int kBSlots = kBPairs * 64;      // histogram columns: (pair, target of 64)
+#ifndef KB_TGT
+#define KB_TGT 64   // targets per CTA: 64 (8 warps, 2 CTAs per SM) or 128 (16 warps, 1 CTA per SM)
+#endif
+constexpr int kBPiv = 4;                   // pivots per CTA (k_group_bound's plane groups)
+constexpr int kBTgt = KB_TGT;              // targets per CTA
+constexpr int kBE = kBTgt / 32;            // 32-target tiles per CTA
+constexpr int kBTE = 2;                    // tiles (targets) per thread
+constexpr int kBTH = kBE / kBTE;           // target halves
+constexpr int kBProb = kBPiv * kBTgt;      // problems per CTA
+constexpr int kBThreads = kBProb;          // one problem per thread in the prologue and epilogue
+constexpr int kBWarps = kBThreads / 32;
+constexpr int kBRG = kBWarps / kBTH;       // row groups (warps per target half)
+constexpr int kBMinBlocks = kBTgt == 64 ? 2 : 1;
 #ifndef KB_ROWS
 #define KB_ROWS 64
-#endif
-#ifndef KB_GUNROLL
-#define KB_GUNROLL 4  // 4-row groups of a chunk unrolled per warp (a 64-row chunk has 4)
 #endif
 #ifndef KB_STAGES
 #define KB_STAGES 2
 #endif
+#ifndef KB_FLUSH
+#define KB_FLUSH (256 / KB_ROWS)  // chunks between FP32 -> FP64 residual flushes (<= 16 pair sums, see below)
+#endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
-constexpr int kBTile = kBRows * 32 * 4;    // one x_ij float tile [row][32 targets]; a stage holds two
-constexpr int kBPlane = kBRows * kBPiv * 12;  // k_group_bound records: 12 B per (row, pivot)
-constexpr int kBStage = 2 * kBTile + kBPlane;
+constexpr int kBRowsW = kBRows / kBRG;     // rows per warp per chunk
+constexpr int kBTile = kBRows * kBTgt * 4;  // the rows' x_ij of the CTA's targets (k_tile_q order)
+constexpr int kBPlane = kBRows * kBPiv * 12;  // k_group_bound records: 48 B per row
+constexpr int kBStage = kBTile + kBPlane;
 constexpr int kBStages = KB_STAGES;
-constexpr int kBGUnroll = KB_GUNROLL;
-constexpr int kBHist = 2 * kNB * kBSlots * 4;  // [pivot of the pair][bin][slot], exact 32-bit sums
+constexpr int kBHist = kBPiv * kNB * kBTgt * 4;  // [pivot][bin][target slot], exact 32-bit sums
 static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
-static_assert(kBRows % (4 * kBQuarters) == 0, "a chunk is whole 4-row groups per quarter");
-static_assert(kBStages * kBStage >= kBQuarters * 4 * kBPairs * 32 * 8, "stage buffers hold the residual shares");
+static_assert(kBTgt == 64 || kBTgt == 128, "k_tile_q lays out 64- or 128-target groups");
+static_assert(kBRowsW % 2 == 0 && kBRows % kBRG == 0, "a warp takes whole row pairs of a chunk");
+static_assert(KB_FLUSH * kBRowsW <= 32, "residual summation margin (column_bounds) covers 16 row pairs");
+static_assert(kBStages * kBStage >= kBRG * kBProb * 8, "stage buffers hold the warps' residual shares");
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 // bracket half-width in sample ranks: narrow for the one-pass bound (tight
 // bins), wider when later passes refine it (fewer optima outside)
@@ -104,7 +116,8 @@ __device__ __forceinline__ void column_bounds(const Prefix& H, double q, double 
   // of its binned position, so f moves by at most pert when the rows are
   // moved into their bins; the bounds below hold for that moved problem
   const double pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
-  // (a chunk sums 16 pairwise 4-row sums: relative error <= 18 u)
+  // (k_bound: each thread's FP32 accumulator takes <= 16 two-row sums between
+  // FP64 flushes, KB_FLUSH: relative error <= 17 u)
   const double eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
   const double fc = ec + lam * fabs(c);
   // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
@@ -273,20 +286,21 @@ __device__ __forceinline__ void sample_bracket1(const SelParams& P, int64_t p, i
                                                 float* smin, float* smax, double lam_lo, double lam_hi, int rep,
                                                 int nrep) {
   const int64_t n = P.n;
-  float sr[kSample], sw[kSample];
-  float wmax = 0.f;
+  // weights quantised to a byte against 4x the pivot's mean weight (they only
+  // steer the bracket), so each key is built as its row arrives
+  const double tw = Tq * unit;
+  const float wsc = tw > 0.0 ? (float)(255.0 * (double)P.nnz[p] / (4.0 * tw)) : 0.f;
+  unsigned key[kSample];
+  // rows (2 (s nrep + rep) + 1) n / (64 nrep), in float (any rows would do;
+  // a 64-bit division by the runtime nrep would cost a register-hungry call)
+  const float rstep = (float)n / (float)(2 * kSample * nrep);
 #pragma unroll
   for (int s = 0; s < kSample; ++s) {
-    const int64_t r = ((2 * ((int64_t)s * nrep + rep) + 1) * n) / (2 * (int64_t)kSample * nrep);
+    const int64_t r = min(n - 1, (int64_t)((float)(2 * (s * nrep + rep) + 1) * rstep));
     const float2 f = P.pf[p * P.np + r];
-    sr[s] = P.Xft[tbase + r * 32 + lane] * f.x;
-    sw[s] = fabsf(f.y);
-    wmax = fmaxf(wmax, sw[s]);
+    const float wq = fminf(255.f, fabsf(f.y) * wsc);
+    key[s] = (f2key(P.Xft[tbase + r * 32 + lane] * f.x) & 0xffffff00u) | (unsigned)__float2uint_rn(wq);
   }
-  const float wsc = wmax > 0.f ? 255.f / wmax : 0.f;
-  unsigned key[kSample];
-#pragma unroll
-  for (int s = 0; s < kSample; ++s) key[s] = (f2key(sr[s]) & 0xffffff00u) | (unsigned)__float2uint_rn(sw[s] * wsc);
 #pragma unroll
   for (int k = 2; k <= kSample; k <<= 1) {
 #pragma unroll
@@ -421,104 +435,68 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
 // the range is the one the previous pass over the same problem left in
 // P.NEXTr (row P.seeds[k] of that pass's pivot list, or k), i.e. where that
 // pass proved the optimum lies, so the 62 bins shrink by ~60x per pass and
-// the integration error with their square.  Every pass also writes the next
-// range (P.NEXTw), the seed range for the exact solver (P.BRK) and the
-// per-column bounds (P.LB / P.UB).
+// the integration error with their square.
 //
-// Threads: a CTA is 4 pivots (2 pairs) x 64 targets (two 32-target tiles of
-// Xft).  Each thread owns FOUR problems: the 2 pivots of its warp's pair x
-// targets (lane, 32 + lane) of the tile pair, so one 16-byte broadcast load
-// of a row pair's plane records serves 2 x 2 x 32 = 128 ratio elements and
-// the shared-memory wavefronts per element drop to 30 / 512 (8 tile loads,
-// 6 record loads, 16 atomics per 4-row group).  The 4 warps of a pair
-// (quarters) split each chunk's rows (4-row groups q, q + 4) and add into the
-// same histograms, so the CTA holds 8 warps for the histogram space of 2.
+// Outputs: every pass adds its column bounds, rounded outward to the
+// fixed-point grid 2^-fxk, into the per-pivot integer sums P.LBq / P.UBq
+// (exact, so independent of the order CTAs finish in; k_bound_finish turns
+// them into per-pivot bounds).  Every pass also writes per problem the next
+// range (P.NEXTw, 8 bytes) and, unless P.lean, the seed range for the exact
+// solver (P.BRK) and the column bounds (P.LB / P.UB): a lean first pass over
+// every pivot skips those 32 bytes per problem (the continuing passes over
+// the few survivors write them).  MULTI: every penalty of P.lams gets its own epilogue (the
+// histogram is penalty-free), the sums go to row l of LBq / UBq and the next
+// ranges (if P.NEXTm) to NEXTm[l].
+//
+// Threads: a CTA is 4 pivots x 128 targets (four 32-target tiles of Xft), 16
+// warps.  Warp w works on target half th = w % 2 (tiles 2 th, 2 th + 1) and
+// rows rg * 4 .. rg * 4 + 3 (rg = w / 2) of every 32-row chunk; a thread owns
+// the eight problems (pivot t, tile e of its half) of its lane and adds into
+// the CTA's histograms ([pivot][bin][e * 32 + lane]: every atomic instruction
+// touches 32 consecutive words, one per bank).  Prologue and epilogue: thread
+// tid prepares and finishes problem q = tid = t * 128 + e * 32 + lane.
 // SPLIT (few pivots, many rows: a grid too small to fill the GPU): the rows
 // are also split over blockIdx.z; every CTA adds its histograms into P.GH
 // (exact integer sums, any order), leaves its residual share in P.GE[z] and
 // (z = 0) the ranges in P.GB, and k_bound_epi finishes each problem.
 template <bool CONT, bool SPLIT, bool MULTI = false, bool TALL = false>
-__global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
+__global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [2 pivots of a pair][kNB][kBSlots]
-  __shared__ __align__(8) unsigned long long full[kBStages];
-  __shared__ unsigned done[kBStages];   // warps finished with the stage's chunk
-  __shared__ float sbr[2][5][kBSlots];  // brackets: problem (t, slot)'s (lo, hi, cen, smin, smax)
+  unsigned* hist = (unsigned*)(smem + kBStages * kBStage);  // [kBPiv][kNB][kBTgt]
+  __shared__ __align__(8) unsigned long long full[kBStages];   // chunk landed (TMA transaction count)
+  __shared__ unsigned done[kBStages];      // warps finished with the stage's chunk
+  __shared__ float sbr[5][kBProb];         // problem q: (lo, hi, cen, smin, smax)
+  __shared__ unsigned long long psum[kBWarps][2];  // per-warp pivot sums (lb, ub)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quarter = warp / kBPairs, pair = warp % kBPairs;
-  const int tq = quarter & 1, eq = quarter >> 1;  // the problem this thread prepares and finishes
+  const int th = warp % kBTH, rg = warp / kBTH;
   const int64_t n = P.n, m = P.m, np = P.np;
-  const int64_t tile0 = (int64_t)blockIdx.x * 2;  // this CTA's two 32-target tiles of Xft
-  const bool tile1 = (tile0 + 1) * 32 < m;         // the second one exists
-  const int64_t gbase = (int64_t)blockIdx.y * np * kBPiv;  // this CTA's pivot group in the plane
+  const int64_t tile0 = (int64_t)blockIdx.x * kBE;            // this CTA's first 32-target tile of Xft
+  const int64_t gbase = (int64_t)blockIdx.y * np;              // this CTA's pivot group in the plane (rows)
 
-  // this thread's own problem (tq, eq): bracketed before the main loop and
-  // finished after it; its metadata is recomputed there instead of living
-  // in registers through the loop
-  const int64_t jq = (tile0 + eq) * 32 + lane;
-  const int slq = pair * 64 + eq * 32 + lane;
-  auto meta = [&](int64_t& k, int64_t& pv, bool& okk, bool& dg, double& T, double& u) {
-    k = (int64_t)blockIdx.y * kBPiv + 2 * pair + tq;
-    okk = k < P.npiv;
-    pv = okk ? pivot_of(P, k) : 0;
+  // the metadata of this thread's epilogue problem q = tid
+  const int qt = tid / kBTgt, qs = tid % kBTgt;  // pivot, target slot (e * 32 + lane)
+  const int64_t qk = (int64_t)blockIdx.y * kBPiv + qt;
+  const int64_t qj = tile0 * 32 + qs;
+  auto meta = [&](int64_t& pv, bool& okk, bool& dg, double& T, double& u) {
+    okk = qk < P.npiv;
+    pv = okk ? pivot_of(P, qk) : 0;
     dg = okk && P.nnz[pv] == 0;
     T = okk && !dg ? P.tq[pv] : 0.0;
     u = ldexp(1.0, okk && !dg ? -P.spow[pv] : 0);
   };
-  bool busy;  // the warp has a live problem
-  {
-    bool any = false;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int64_t k = (int64_t)blockIdx.y * kBPiv + 2 * pair + t;
-      const bool okk = k < P.npiv;
-      const int64_t pv = okk ? pivot_of(P, k) : 0;
-      const bool dg = okk && P.nnz[pv] == 0;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t jj = (tile0 + e) * 32 + lane;
-        any |= okk && !dg && jj < m && jj != pv;
-      }
-    }
-    busy = __any_sync(0xffffffffu, any);
-  }
-  {  // each quarter prepares one of the four problems' brackets; all need all
-    float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
-    int64_t k, pv;
-    bool okk, dg;
-    double T, u;
-    meta(k, pv, okk, dg, T, u);
-    if (okk && !dg && jq < m && jq != pv) {
-      if (CONT) {
-        const float2 r = P.NEXTr[(P.seeds ? P.seeds[k] : k) * m + jq];
-        b0 = b3 = r.x;
-        b1 = b4 = r.y;
-        b2 = 0.5f * (r.x + r.y);
-      } else {
-        sample_bracket<TALL>(P, pv, (tile0 + eq) * np * 32, lane, T, u, P.delta, &b0, &b1, &b2, &b3, &b4,
-                       MULTI ? P.lams[0] : lam_of(P, k), MULTI ? P.lams[P.nlam - 1] : lam_of(P, k));
-      }
-    }
-    float* d = &sbr[tq][0][slq];
-    d[0] = b0;
-    d[kBSlots] = b1;
-    d[2 * kBSlots] = b2;
-    d[3 * kBSlots] = b3;
-    d[4 * kBSlots] = b4;
-  }
   const int64_t nall = (n + kBRows - 1) / kBRows;
   const int64_t cb = SPLIT ? nall * blockIdx.z / gridDim.z : 0;  // this CTA's chunks [cb, cb + nch)
   const int64_t nch = SPLIT ? nall * (blockIdx.z + 1) / gridDim.z - cb : nall;
   // stage refill: local chunk c (global cb + c) goes to stage c % kBStages
+  // (no proxy fence in the loop: the ring is only ever read by generic
+  // loads there, and a fence would drain the issuing warp's histogram atomics)
   auto issue = [&](int64_t c) {
     const int st = (int)(c % kBStages);
     const int64_t i0 = (cb + c) * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
-    fence_proxy_async();
-    mbar_expect_tx(&full[st], (unsigned)(tile1 ? kBStage : kBStage - kBTile));
-    bulk_g2s(base, P.Xft + tile0 * np * 32 + i0 * 32, kBTile, &full[st]);
-    if (tile1) bulk_g2s(base + kBTile, P.Xft + (tile0 + 1) * np * 32 + i0 * 32, kBTile, &full[st]);
-    bulk_g2s(base + 2 * kBTile, P.gbp + (gbase + i0 * kBPiv) * 3 / 4, kBPlane, &full[st]);
+    mbar_expect_tx(&full[st], (unsigned)(kBTile + kBPlane));
+    bulk_g2s(base, P.Xq + ((int64_t)blockIdx.x * np + i0) * kBTgt, kBTile, &full[st]);
+    bulk_g2s(base + kBTile, P.gbp + (gbase + i0) * 3, kBPlane, &full[st]);
   };
   if (tid == 0) {
     for (int s = 0; s < kBStages; ++s) {
@@ -526,100 +504,129 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
       done[s] = 0u;
     }
     mbar_fence_init();
+    fence_proxy_async();
     for (int64_t c = 0; c < min((int64_t)kBStages, nch); ++c) issue(c);
   }
-  for (int x = tid; x < 2 * kNB * kBSlots; x += kBThreads) hist[x] = 0u;
-  __syncthreads();
-  float cf[2][2], A[2][2], B[2][2];
-  unsigned hb[2][2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int sl = pair * 64 + e * 32 + lane;
-      const float l = sbr[t][0][sl], h = sbr[t][1][sl];
-      cf[t][e] = sbr[t][2][sl];
-      A[t][e] = (62.f / 63.f) / (h - l);
-      B[t][e] = 0.5f / 63.f - l * A[t][e];
-      hb[t][e] = smem_u32(hist + t * kNB * kBSlots + sl) - 0x4B000000u * (unsigned)(kBSlots * 4);
+  {  // bracket of problem tid while the first chunks are in flight
+    float b0 = -1.f, b1 = 1.f, b2 = 0.f, b3 = -1.f, b4 = 1.f;
+    int64_t pv;
+    bool okk, dg;
+    double T, u;
+    meta(pv, okk, dg, T, u);
+    if (okk && !dg && qj < m && qj != pv) {
+      if (CONT) {
+        const float2 r = P.NEXTr[(P.seeds ? P.seeds[qk] : qk) * m + qj];
+        b0 = b3 = r.x;
+        b1 = b4 = r.y;
+        b2 = 0.5f * (r.x + r.y);
+      } else {
+        sample_bracket<TALL>(P, pv, (qj >> 5) * np * 32, lane, T, u, P.delta, &b0, &b1, &b2, &b3, &b4,
+                             MULTI ? P.lams[0] : lam_of(P, qk), MULTI ? P.lams[P.nlam - 1] : lam_of(P, qk));
+      }
     }
+    sbr[0][tid] = b0;
+    sbr[1][tid] = b1;
+    sbr[2][tid] = b2;
+    sbr[3][tid] = b3;
+    sbr[4][tid] = b4;
   }
+  for (int x = tid; x < kBPiv * kNB * kBTgt; x += kBThreads) hist[x] = 0u;
+  __syncthreads();
+  // this thread's eight problems: bin map t = sat(r A + B) (63 t + 2^23 has
+  // the bin in its low bits), residual reference point c
+  float A[kBPiv][kBTE], B[kBPiv][kBTE];
+  float2 nc[kBPiv / 2][kBTE];  // (-c_{2h}, -c_{2h+1}) as a register pair for FFMA2
+#pragma unroll
+  for (int t = 0; t < kBPiv; ++t)
+#pragma unroll
+    for (int ee = 0; ee < kBTE; ++ee) {
+      const int q = t * kBTgt + (th * kBTE + ee) * 32 + lane;
+      const float l = sbr[0][q], hh = sbr[1][q];
+      A[t][ee] = (62.f / 63.f) / (hh - l);
+      B[t][ee] = 0.5f / 63.f - l * A[t][ee];
+      if (t & 1) nc[t >> 1][ee].y = -sbr[2][q];
+      else nc[t >> 1][ee].x = -sbr[2][q];
+    }
+  // bin b of (t, e) -> hist + ((t * kNB + b) * kBTgt + e * 32 + lane) words;
+  // 63 t + 2^23 has bits 0x4B000000 + b
+  const unsigned hb = smem_u32(hist + th * kBTE * 32 + lane) - 0x4B000000u * (unsigned)(kBTgt * 4);
 
   unsigned fphase = 0;
-  double ec[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // this quarter's share of e_j(c) of the four problems
+  float racc[kBPiv][kBTE];
+  double ec[kBPiv][kBTE];  // this warp's share of e_j(c) of the eight problems
+#pragma unroll
+  for (int t = 0; t < kBPiv; ++t)
+#pragma unroll
+    for (int ee = 0; ee < kBTE; ++ee) {
+      racc[t][ee] = 0.f;
+      ec[t][ee] = 0.0;
+    }
+  int nflush = 0;
   for (int64_t c = 0; c < nch; ++c) {
     const int st = (int)(c % kBStages);
     mbar_wait(&full[st], (fphase >> st) & 1u);
     fphase ^= 1u << st;
-    if (busy) {
-      const unsigned char* sb = smem + (size_t)st * kBStage;
-      const float* ta = (const float*)sb;  // [2 tiles][kBRows][32]
-      // records of this warp's pivot pair: 3 float4 per row pair and pivot pair
-      const float4* rec = (const float4*)(sb + 2 * kBTile) + pair * 3;
-      float racc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll kBGUnroll
-      for (int r0 = 4 * quarter; r0 < kBRows; r0 += 4 * kBQuarters) {
-        float av[2][4];
-        float4 yw[4];  // (y0, x0, y1, x1) of row r0 + u
-        uint2 wu[4];
+    const unsigned char* sb = smem + (size_t)st * kBStage;
+    const float2* ta = (const float2*)sb + th * 32 + lane;  // [kBRows][half][lane]: this thread's two targets
+    const float4* rec = (const float4*)(sb + kBTile);       // [kBRows][3]
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+    for (int u2 = 0; u2 < kBRowsW; u2 += 2) {
+      float rp[2][kBPiv][kBTE];  // x_ij - c x_ip of the row pair
 #pragma unroll
-          for (int u = 0; u < 4; ++u) av[e][u] = ta[e * kBRows * 32 + (r0 + u) * 32 + lane];
+      for (int v = 0; v < 2; ++v) {
+        const int r = rg * kBRowsW + u2 + v;
+        static_assert(kBTE == 2, "one 8-byte load per row");
+        const float2 xv = ta[r * (kBTgt / 2)];
+        const float x[kBTE] = {xv.x, xv.y};
+        const float4 Y = rec[r * 3], X = rec[r * 3 + 1], W = rec[r * 3 + 2];
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {  // row pairs (r0, r0+1), (r0+2, r0+3)
-          const float4* rp = rec + ((r0 >> 1) + h2) * (kBPairs * 3);
-          const float4 L0 = rp[0], L1 = rp[1], L2 = rp[2];
-          yw[2 * h2] = make_float4(L0.x, L0.z, L0.y, L0.w);
-          wu[2 * h2] = make_uint2(__float_as_uint(L1.x), __float_as_uint(L1.y));
-          yw[2 * h2 + 1] = make_float4(L1.z, L2.x, L1.w, L2.y);
-          wu[2 * h2 + 1] = make_uint2(__float_as_uint(L2.z), __float_as_uint(L2.w));
+        for (int h = 0; h < kBPiv / 2; ++h) {
+          const float2 yy = h ? make_float2(Y.z, Y.w) : make_float2(Y.x, Y.y);
+          const float2 xx = h ? make_float2(X.z, X.w) : make_float2(X.x, X.y);
+          const unsigned w0 = __float_as_uint(h ? W.z : W.x), w1 = __float_as_uint(h ? W.w : W.y);
+#pragma unroll
+          for (int ee = 0; ee < kBTE; ++ee) {
+            const float2 q = fmul2(make_float2(x[ee], x[ee]), yy);
+            const float2 bb = ffma2(make_float2(__saturatef(fmaf(q.x, A[2 * h][ee], B[2 * h][ee])),
+                                                __saturatef(fmaf(q.y, A[2 * h + 1][ee], B[2 * h + 1][ee]))),
+                                    make_float2(63.f, 63.f), make_float2(8388608.f, 8388608.f));
+            const unsigned a0 = hb + __float_as_uint(bb.x) * (unsigned)(kBTgt * 4) +
+                                (unsigned)(((2 * h) * kNB * kBTgt + ee * 32) * 4);
+            const unsigned a1 = hb + __float_as_uint(bb.y) * (unsigned)(kBTgt * 4) +
+                                (unsigned)(((2 * h + 1) * kNB * kBTgt + ee * 32) * 4);
+            // fire-and-forget shared adds (the other warps add into the same bins)
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(w0));
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1), "r"(w1));
+            // x_ij - c x_ip (dropped rows: x_ij)
+            const float2 rr = ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee]));
+            rp[v][2 * h][ee] = rr.x;
+            rp[v][2 * h + 1][ee] = rr.y;
+          }
         }
-        // both pivots of the pair at once (packed pairs; same bits as scalar)
-        unsigned a0[2][4], a1[2][4];
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float2 q = fmul2(make_float2(av[e][u], av[e][u]), make_float2(yw[u].x, yw[u].z));
-            const float2 b = ffma2(make_float2(__saturatef(fmaf(q.x, A[0][e], B[0][e])),
-                                               __saturatef(fmaf(q.y, A[1][e], B[1][e]))),
-                                   make_float2(63.f, 63.f), make_float2(8388608.f, 8388608.f));
-            a0[e][u] = hb[0][e] + __float_as_uint(b.x) * (unsigned)(kBSlots * 4);
-            a1[e][u] = hb[1][e] + __float_as_uint(b.y) * (unsigned)(kBSlots * 4);
-          }
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {  // |a - c b| (dropped rows: |a|), pairwise within the 4 rows
-          float e0[4], e1[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float2 r = ffma2(make_float2(-cf[0][e], -cf[1][e]), make_float2(yw[u].y, yw[u].w),
-                                   make_float2(av[e][u], av[e][u]));
-            e0[u] = fabsf(r.x);
-            e1[u] = fabsf(r.y);
-          }
-          racc[0][e] += (e0[0] + e0[1]) + (e0[2] + e0[3]);
-          racc[1][e] += (e1[0] + e1[1]) + (e1[2] + e1[3]);
-        }
-        // fire-and-forget shared adds (the other quarters add into the same bins)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0[e][u]), "r"(wu[u].x));
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1[e][u]), "r"(wu[u].y));
-          }
       }
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
+      for (int t = 0; t < kBPiv; ++t)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) ec[t][e] += (double)racc[t][e];
+        for (int ee = 0; ee < kBTE; ++ee) racc[t][ee] += fabsf(rp[0][t][ee]) + fabsf(rp[1][t][ee]);
+    }
+    if (++nflush == KB_FLUSH || c + 1 == nch) {
+      nflush = 0;
+#pragma unroll
+      for (int t = 0; t < kBPiv; ++t)
+#pragma unroll
+        for (int ee = 0; ee < kBTE; ++ee) {
+          ec[t][ee] += (double)racc[t][ee];
+          racc[t][ee] = 0.f;
+        }
     }
     __syncwarp();
     if (lane == 0) {
-      // the last warp done with the stage refills it (no producer waits)
+      // the last warp done with the stage refills it (no producer waits).
+      // Relaxed: this warp's loads of the stage have all returned (their
+      // values fed the arithmetic above), and a release here would also
+      // wait for the warp's in-flight histogram atomics every chunk.
       unsigned old;
-      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
                    : "=r"(old)
                    : "r"(smem_u32(&done[st]))
                    : "memory");
@@ -630,85 +637,124 @@ __global__ void __launch_bounds__(kBThreads, 2) k_bound(SelParams P) {
     }
   }
   // every chunk has been waited for, so no bulk copy is in flight: the stage
-  // buffers carry the quarters' residual shares to the problem's finisher
-  __syncthreads();  // also: every quarter's histogram adds are in
-  double* ecx = (double*)smem;  // [quarter][t][e][pair][lane]
+  // buffers carry the row groups' residual shares to the problems' finishers
+  __syncthreads();  // also: every warp's histogram adds are in
+  double* ecx = (double*)smem;  // [row group][q]
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
+  for (int t = 0; t < kBPiv; ++t)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) ecx[((quarter * 2 + t) * 2 + e) * (kBPairs * 32) + pair * 32 + lane] = ec[t][e];
+    for (int ee = 0; ee < kBTE; ++ee) ecx[rg * kBProb + t * kBTgt + (th * kBTE + ee) * 32 + lane] = ec[t][ee];
   __syncthreads();
+  const int fx = P.fxk ? *P.fxk : 0;
   double ect = 0.0;
 #pragma unroll
-  for (int q = 0; q < kBQuarters; ++q) ect += ecx[((q * 2 + tq) * 2 + eq) * (kBPairs * 32) + pair * 32 + lane];
-  const int64_t jj = jq;
-  const int sl = slq;
-  const float tlo = sbr[tq][0][sl], thi = sbr[tq][1][sl], tcf = sbr[tq][2][sl];
-  int64_t kq, pq;
-  bool okq, dgq;
-  double Tqq, utq;
-  meta(kq, pq, okq, dgq, Tqq, utq);
+  for (int g = 0; g < kBRG; ++g) ect += ecx[g * kBProb + tid];
+  const float tlo = sbr[0][tid], thi = sbr[1][tid], tcf = sbr[2][tid];
+  // per-pivot fixed-point sums of one penalty's column bounds (lb rounded
+  // down, ub up; both clamped to the column's f(0) bound, which keeps lb a
+  // lower bound and the sums below 2^61): warp sums, then the pivot's four
+  // warps in a fixed order, one integer atomic per (pivot, CTA)
+  auto pivot_sums = [&](double lb, double ub, int64_t row) {
+    unsigned long long ql = 0, qu = 0;
+    if (P.LBq) {
+      ql = (unsigned long long)__double2ull_rd(ldexp(lb, fx));
+      qu = (unsigned long long)__double2ull_ru(ldexp(ub, fx));
+    }
+    for (int o = 16; o; o >>= 1) {
+      ql += __shfl_xor_sync(0xffffffffu, ql, o);
+      qu += __shfl_xor_sync(0xffffffffu, qu, o);
+    }
+    if (lane == 0) {
+      psum[warp][0] = ql;
+      psum[warp][1] = qu;
+    }
+    __syncthreads();
+    constexpr int WP = kBWarps / kBPiv;  // warps per pivot (q = tid: pivot t = warp / WP)
+    if (P.LBq && tid < kBPiv) {
+      const int64_t k = (int64_t)blockIdx.y * kBPiv + tid;
+      if (k < P.npiv) {
+        unsigned long long sl = 0, su = 0;
+        for (int w = tid * WP; w < (tid + 1) * WP; ++w) {
+          sl += psum[w][0];
+          su += psum[w][1];
+        }
+        atomicAdd(&P.LBq[row * P.npiv + k], sl);
+        atomicAdd(&P.UBq[row * P.npiv + k], su);
+      }
+    }
+    __syncthreads();
+  };
+  int64_t pv;
+  bool okk, dg;
+  double T, u;
+  meta(pv, okk, dg, T, u);
+  const bool live = okk && qj < m && !dg && qj != pv;
   if (MULTI) {
-    // every penalty in P.lams (ascending): the column bounds summed over the
-    // warp's 32 targets (one pivot), one atomic per warp and penalty
-    const bool live = okq && jj < m && !dgq && jj != pq;
-    Prefix H{hist + tq * kNB * kBSlots + sl, kBSlots};
+    Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
     H.build();  // once for every penalty
     for (int l = 0; l < P.nlam; ++l) {
       double lb = 0.0, ub = 0.0;
       float2 nx = make_float2(tlo, thi);
       if (live) {
-        double2 rg;
-        column_bounds(H, ldexp(utq, 21), (double)tlo, (double)thi, (double)tcf, ect, Tqq * utq,
-                      P.lams[l], P.colsum[jj], n, sbr[tq][3][sl], sbr[tq][4][sl], &lb, &ub, &rg, &nx);
-      } else if (okq && jj < m && dgq) {
-        lb = ub = P.colsum[jj];  // fit.py:66-72: v = 0, error = sum |x|
+        double2 rg2;
+        column_bounds(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u, P.lams[l],
+                      P.colsum[qj], n, sbr[3][tid], sbr[4][tid], &lb, &ub, &rg2, &nx);
+        ub = fmin(ub, P.colsum[qj] * (1.0 + 0x1p-20));
+        lb = fmin(lb, ub);
+      } else if (okk && qj < m && dg) {
+        lb = ub = P.colsum[qj];  // fit.py:66-72: v = 0, error = sum |x|
       }
       // each penalty's next range, for a continuing pass per (penalty, pivot) entry
-      if (P.NEXTm && okq && jj < m) P.NEXTm[((int64_t)l * P.npiv + kq) * m + jj] = nx;
-      lb = warp_sum(lb);
-      ub = warp_sum(ub);
-      if (lane == 0 && okq) {
-        atomicAdd(&P.LBm[l * P.npiv + kq], lb);
-        atomicAdd(&P.UBm[l * P.npiv + kq], ub);
+      if (P.NEXTm && okk && qj < m) P.NEXTm[((int64_t)l * P.npiv + qk) * m + qj] = nx;
+      pivot_sums(lb, ub, l);
+    }
+    return;
+  }
+  double lbv = 0.0, ubv = 0.0;
+  if (okk && qj < m) {
+    const int64_t o = qk * m + qj;
+    if (SPLIT) {
+      const unsigned* hc = hist + qt * kNB * kBTgt + qs;
+      for (int b = 0; b < kNB; ++b) {
+        const unsigned x = hc[b * kBTgt];
+        if (x) atomicAdd(&P.GH[o * kNB + b], x);
+      }
+      P.GE[(int64_t)blockIdx.z * P.npiv * m + o] = ect;
+      if (blockIdx.z == 0) {
+        float* g = P.GB + o * 5;
+        g[0] = tlo;
+        g[1] = thi;
+        g[2] = tcf;
+        g[3] = sbr[3][tid];
+        g[4] = sbr[4][tid];
+      }
+    } else if (!live) {
+      const double z = dg ? P.colsum[qj] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
+      lbv = ubv = z;
+      P.NEXTw[o] = make_float2(tlo, thi);
+      if (!P.lean) {
+        P.LB[o] = z;
+        P.UB[o] = z;
+        P.BRK[o] = make_double2(-INFINITY, INFINITY);
+      }
+    } else {
+      double2 rg2;
+      float2 nx;
+      Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
+      H.build();
+      column_bounds(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u, lam_of(P, qk),
+                    P.colsum[qj], n, sbr[3][tid], sbr[4][tid], &lbv, &ubv, &rg2, &nx);
+      ubv = fmin(ubv, P.colsum[qj] * (1.0 + 0x1p-20));
+      lbv = fmin(lbv, ubv);
+      P.NEXTw[o] = nx;
+      if (!P.lean) {
+        P.LB[o] = lbv;
+        P.UB[o] = ubv;
+        P.BRK[o] = rg2;
       }
     }
-    return;
   }
-  if (jj >= m || !okq) return;
-  const int64_t o = kq * m + jj;
-  if (SPLIT) {
-    const unsigned* hc = hist + tq * kNB * kBSlots + sl;
-    for (int b = 0; b < kNB; ++b) {
-      const unsigned x = hc[b * kBSlots];
-      if (x) atomicAdd(&P.GH[o * kNB + b], x);
-    }
-    P.GE[(int64_t)blockIdx.z * P.npiv * m + o] = ect;
-    if (blockIdx.z == 0) {
-      float* g = P.GB + o * 5;
-      g[0] = tlo;
-      g[1] = thi;
-      g[2] = tcf;
-      g[3] = sbr[tq][3][sl];
-      g[4] = sbr[tq][4][sl];
-    }
-    return;
-  }
-  if (dgq || jj == pq) {
-    const double z = dgq ? P.colsum[jj] : 0.0;  // fit.py:66-72: v = 0, error = sum |x|
-    P.LB[o] = z;
-    P.UB[o] = z;
-    P.BRK[o] = make_double2(-INFINITY, INFINITY);
-    P.NEXTw[o] = make_float2(tlo, thi);
-    return;
-  }
-  double lb, ub;
-  Prefix H{hist + tq * kNB * kBSlots + sl, kBSlots};
-  H.build();
-  column_bounds(H, ldexp(utq, 21), (double)tlo, (double)thi, (double)tcf, ect, Tqq * utq,
-                lam_of(P, kq), P.colsum[jj], n, sbr[tq][3][sl], sbr[tq][4][sl], &lb, &ub, &P.BRK[o], &P.NEXTw[o]);
-  P.LB[o] = lb;
-  P.UB[o] = ub;
+  if (!SPLIT) pivot_sums(lbv, ubv, 0);
 }
 
 // Epilogue of a SPLIT k_bound: thread per (pivot, target) problem, the
@@ -739,12 +785,14 @@ __global__ void k_bound_epi(SelParams P, int nsplit) {
   P.UB[o] = ub;
 }
 
-// Penalty of v_p = 1 for every pivot and penalty of a multi-penalty pass.
+// Per-pivot bounds from k_bound's fixed-point sums (rounded outward) plus
+// the penalty of v_p = 1, for every pivot and penalty of the pass.
 __global__ void k_bound_finish(SelParams P, double* __restrict__ lb, double* __restrict__ ub) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.npiv * P.nlam) return;
   const int64_t l = t / P.npiv, kk = t - l * P.npiv;
-  const double pen = P.nnz[pivot_of(P, kk)] ? P.lams[l] : 0.0;
-  lb[t] += pen;
-  ub[t] += pen;
+  const int fx = *P.fxk;
+  const double pen = P.nnz[pivot_of(P, kk)] ? (P.lams ? P.lams[l] : lam_of(P, kk)) : 0.0;
+  lb[t] = __dadd_rd(ldexp(__ull2double_rd(P.LBq[t]), -fx), pen);
+  ub[t] = __dadd_ru(ldexp(__ull2double_ru(P.UBq[t]), -fx), pen);
 }

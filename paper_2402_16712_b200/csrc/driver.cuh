@@ -82,8 +82,10 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
   std::vector<double> lb(npiv), ub(npiv);
   int64_t nfit;
   if (do_prune) {
+    // lean: per-pivot bound sums and next ranges only (the continuing passes
+    // over the survivors write their seeds and column bounds)
     st = fit_impl(d_X, n, m, &lam, 1, p_begin, p_stride, nullptr, npiv, true, nullptr, nullptr, nullptr, nullptr,
-                  d_lb, d_ub, d_ws, ws_bytes, stream, 1);
+                  d_lb, d_ub, d_ws, ws_bytes, stream, 1, nullptr, 0, nullptr, nullptr, nullptr, /*lean=*/true);
     if (st != L1B_OK) return st;
     if (cudaMemcpyAsync(lb.data(), d_lb, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaMemcpyAsync(ub.data(), d_ub, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
@@ -98,7 +100,11 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
     seed_n = npiv;
     std::vector<int64_t> list(keep.size());
     for (size_t i = 0; i < keep.size(); ++i) list[i] = piv[keep[i]];
-    for (int level = 0; level < kRefinePasses && (int64_t)list.size() > kRefineMin; ++level) {
+    // at least one continuing pass: the lean pass left no exact-solver seeds
+    bool seeded_ranges = false;
+    for (int level = 0; level < kRefinePasses && !list.empty() && (!seeded_ranges || (int64_t)list.size() > kRefineMin);
+         ++level) {
+      seeded_ranges = true;
       const int64_t c = (int64_t)list.size();
       st = fit_impl(d_X, n, m, &lam, 1, 0, 1, list.data(), c, true, nullptr, nullptr, nullptr, nullptr, d_lb, d_ub,
                     d_ws, ws_bytes, stream, 1, seed.data(), seed_n);

@@ -43,6 +43,7 @@ constexpr double kBig = 1.7976931348623157e308;  // DBL_MAX: open window side
 struct SelParams {
   const double* Xt;      // X in 32-column tiles: ((j/32)*np + i)*32 + j%32
   const float* Xft;      // float copy of Xt
+  const float* Xq;       // k_bound's 128-target tiles (k_tile_q)
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
   const unsigned* gwu;   // shard wq_ip / 2^21 (rounded) in 8-pivot groups
@@ -91,6 +92,10 @@ struct SelParams {
   float2* NEXTm;         // multi-penalty bound: next ranges [nlam][npiv][m] (optional)
   double* LBm;           // multi-penalty bound: per (penalty, pivot) sums [nlam][npiv]
   double* UBm;
+  unsigned long long* LBq;  // k_bound: per (penalty, pivot) column-bound sums, fixed point 2^-fxk ([nlam][npiv])
+  unsigned long long* UBq;
+  const int* fxk;        // fixed-point exponent (k_fxscale)
+  int lean;              // k_bound: per-pivot sums only (no per-problem LB / UB / BRK / NEXT records)
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {
