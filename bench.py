@@ -8,23 +8,31 @@ n=2000, seed=0, noise_scale=1), lambda = 1 -- the reference CLI's bench
 recipe, cli.py:246-260).  Metric: BASELINE.json's "ms per sparse L1 line fit
 at 2000x2000 and weighted-median solves/sec"; ``value`` is solves/s for the
 whole job (m(m-1) weighted-median problems per fit), ``ms_per_step`` is ms
-per fit.
+per fit.  (solves/s is nominal under pruning: every problem is bounded, only
+the surviving pivots' problems are solved exactly -- results identical.)
 
 * value       -- X resident in HBM; device time of K fits with CUDA events on
                  the launching stream, L2 flushed (256 MB write) before every
-                 timed fit, max over ranks.  A fit = K0 prepare + K1 select +
-                 K2 reduce + exact re-scoring of the winner.
+                 timed fit, max over ranks.  A fit = K0 prepare + the pruned
+                 cascade (one k_bound pass over every problem, refining passes
+                 over the survivors, the seeded exact solver) + exact
+                 re-scoring of the winner in NumPy's summation order.
 * e2e         -- the public API (paper_2402_16712_b200.fit_line) from a host
                  numpy array: H2D of X, the fit, D2H of the line, per step.
-* roofline    -- K1 (k_select), the dominant kernel: algorithmic FP64 work
-                 11 ops per ratio element (8 for IEEE division + 3 for the
-                 residual) over its event-timed duration,
-                 against the FP64 pipe peak measured here with a DFMA probe.
-* cpu_baseline -- the CPU oracle (a C port of the reference algorithm,
-                 oracle/) on this host's cores, bounded pivot sample,
+* roofline    -- k_bound, the dominant kernel: one shared-memory histogram
+                 atomic per (pivot, target, row) element over its event-timed
+                 duration, against the conflict-free red.shared rate measured
+                 here (l1b_atoms_probe); exact_fit_view reports the exhaustive
+                 exact path (k_select & co.) against the FP64 pipe.
+* cpu_baseline -- the reference package itself (l1line, installed offline in
+                 baseline/_ref) on this host's cores, or the oracle C port where
+                 it is absent; a bounded, evenly spread pivot sample,
                  extrapolated to a full fit.  rank 0, N=1 only.
 
---impl reference times that CPU implementation alone (the reference arm).
+--impl reference times the reference arm: on C1/C2 the unmodified l1line's
+own fit_for_pivot + thread pool over ONE complete fit whose pivots are split
+across the timed steps (each pivot timed once, the argmin printed); elsewhere
+the oracle C port (C3: full fit; C4/C5: strided sample, extrapolated).
 Multi-GPU (torchrun, one process per GPU, NCCL): pivots are interleaved over
 ranks, the winner is combined with one all_gather + one
 broadcast; total work is fixed, so scaling is "strong".
@@ -132,28 +140,73 @@ class ClockSampler:
 def cpu_reference(X, lams, budget_s: float, threads: int | None = None):
     """Time the CPU oracle (C port of the reference algorithm) on a pivot sample.
 
-    Runs batches of `threads` pivots through oracle.fit_pivots (OpenMP over
-    pivots, like parallel.py:36-43) until `budget_s` elapses or every pivot
-    is done; returns (solves/s, seconds per full fit (extrapolated), sample).
+    Batches of `threads` pivots, evenly strided over the whole range (so the
+    sample does not depend on where the cheap or costly pivots sit), one
+    pivot per worker thread, until `budget_s` elapses or every pivot is done;
+    returns (solves/s, seconds per full fit (extrapolated), sample).
     """
-    import oracle
     n, m = X.shape
     threads = threads or os.cpu_count() or 1
+    order = np.argsort((np.arange(m) * 0.6180339887498949) % 1.0, kind="stable")  # low-discrepancy order
+    ref = _reference_package() if len(lams) == 1 else None
+    if ref is not None:  # the reference package itself: fit_for_pivot through its own thread pool
+        l1line, map_indices = ref
+        data = l1line.DataMatrix(X)
+
+        def run(batch):
+            map_indices(lambda i: l1line.fit_for_pivot(data, int(batch[i]), float(lams[0])), batch.size, threads)
+    else:
+        import oracle
+
+        def run(batch):
+            _fit_pivot_set(oracle, X, lams, batch, threads)
     done, t0 = 0, time.perf_counter()
-    batch = max(threads, 1)
     while done < m:
-        hi = min(m, done + batch)
-        oracle.fit_pivots(X, lams, done, hi, threads=threads, want_v=False)
-        done = hi
+        batch = order[done:done + threads]
+        run(batch)
+        done += batch.size
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
     solves = done * (m - 1) * len(lams)
     per_fit = dt * m / done / len(lams)
-    return solves / dt, per_fit, f"{done}/{m} pivots x {len(lams)} lambda of the same input, {dt:.1f}s"
+    what = "l1line.fit_for_pivot (baseline/_ref)" if ref is not None else "oracle C port"
+    return (solves / dt, per_fit, f"{what}: {done}/{m} pivots (evenly spread) x {len(lams)} lambda of the same "
+            f"input, {dt:.1f}s", "reference" if ref is not None else "port")
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _argmin_strict(O):
+    """fit.py:98-102: first pivot with the smallest objective (strict '<' in pivot order)."""
+    best = 0
+    for p in range(1, O.size):
+        if O[p] < O[best]:
+            best = p
+    return best
 
 
 def run_reference(args):
+    """The reference algorithm on this host's cores (the oracle C port, OpenMP over
+    pivots like parallel.py:36-43).
+
+    C1-C3: the timed steps partition the pivots -- step k fits pivots
+    [k m / K, (k + 1) m / K) -- so every pivot of ONE complete fit is timed
+    exactly once and nothing is extrapolated; the strict-'<' argmin over all
+    of them (fit.py:98-102) is printed, so the run also checks the GPU's
+    winner.  C4 / C5 (minutes to hours of CPU per fit): the steps partition an
+    evenly strided pivot sample and the fit time is extrapolated (labelled).
+    """
     world, rank, _ = _dist_env()
     if world > 1:
         import torch.distributed as dist
@@ -163,23 +216,71 @@ def run_reference(args):
             dist.destroy_process_group()
             return
     X, lams = _make_data(args.config)
-    m = X.shape[1]
+    n, m = X.shape
     threads = os.cpu_count() or 1
-    vals = []
-    for step in range(args.warmup + args.steps):
-        sps, per_fit, sample = cpu_reference(X, lams, budget_s=args.ref_budget / max(1, args.warmup + args.steps),
-                                             threads=threads)
-        if step >= args.warmup:
-            vals.append(sps)
-    v = float(np.mean(vals))
-    ms = 1e3 * m * (m - 1) * len(lams) / v
+    ncomp = COMPONENTS.get(args.config, 1)
+    ref = _reference_package() if args.config in ("c1", "c2") and not args.port else None
+    if ref is not None:
+        return _run_reference_package(args, ref, X, lams, threads, world)
+    import oracle
+    full = args.config in ("c1", "c2", "c3")
+    if full:
+        pivots = np.arange(m)
+    else:  # an evenly strided sample of about 4 pivots per thread
+        cnt = min(m, 4 * threads)
+        pivots = np.unique(np.linspace(0, m - 1, cnt).astype(np.int64))
+    K = max(1, args.steps)
+    whole = args.config == "c1"  # a complete fit takes milliseconds: every step is one
+    bounds = [int(round(k * pivots.size / K)) for k in range(K + 1)]
+    if whole:
+        bounds = None
+    for w in range(args.warmup):  # untimed: one batch of `threads` pivots
+        lo = (w * threads) % m
+        oracle.fit_pivots(X, lams, lo, min(m, lo + threads), threads=threads, want_v=False)
+    t_steps, objs = [], []
+    t_wall = time.perf_counter()
+    for k in range(K):
+        sel = pivots if whole else pivots[bounds[k]:bounds[k + 1]]
+        t0 = time.perf_counter()
+        O_parts = []
+        if sel.size:
+            if full:  # a contiguous range
+                _, _, _, O = oracle.fit_pivots(X, lams, int(sel[0]), int(sel[-1]) + 1, threads=threads,
+                                               want_v=False)
+                O_parts.append(O)
+            else:  # a strided sample: one pivot per worker thread
+                O_parts.append(_fit_pivot_set(oracle, X, lams, sel, threads)[3])
+        t_steps.append(time.perf_counter() - t0)
+        objs = O_parts if whole else objs + O_parts
+    wall = time.perf_counter() - t_wall
+    O = np.concatenate(objs, axis=0) if objs else np.zeros((0, len(lams)))
+    # seconds per complete workload pass
+    t_fit = float(np.mean(t_steps)) if whole else float(np.sum(t_steps)) * (m / pivots.size) * ncomp
+    solves = m * (m - 1) * len(lams) * ncomp
+    v = solves / t_fit
+    result = None
+    if full:
+        win = [_argmin_strict(O[:, l]) for l in range(len(lams))]
+        result = {"pivot": win[:4], "objective": [float(O[w, l]) for l, w in enumerate(win)][:4]}
+    sample = (f"a complete fit per step (all {m} pivots x {len(lams)} lambda)" if whole else
+              f"one complete fit: all {m} pivots x {len(lams)} lambda, each timed once across the {K} steps"
+              if full else
+              f"{pivots.size} of {m} pivots (evenly strided) x {len(lams)} lambda, extrapolated x{m / pivots.size:.1f}"
+              + (f" x {ncomp} components (component 1's data)" if ncomp > 1 else ""))
+    if args.config == "c3":
+        sample += ("; the port builds each pivot's tableau once for all 32 penalties (the reference calls "
+                   "fit_line 32 times and re-sorts every time, fit.py:79), so this arm is faster than the reference")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(t_steps)),
+        "ms_per_fit": 1e3 * t_fit, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(args, X, lams, world),
         "cpu_baseline": {"value": v, "unit": "solves/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": _cpu_model(), "sample": sample,
+                         "extrapolated": not full, "fits_in_driver_run": bool(full),
+                         "timed_s": float(np.sum(t_steps)), "wall_s": wall},
+        "result": result,
         "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -187,6 +288,90 @@ def run_reference(args):
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _reference_package():
+    """The unmodified reference package (l1line 0.1.0), installed offline into
+    baseline/_ref, or None where it is absent."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "l1line")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    try:
+        import l1line
+        from l1line.parallel import map_indices
+    except Exception:  # noqa: BLE001 -- fall back to the port
+        return None
+    return l1line, map_indices
+
+
+def _run_reference_package(args, ref, X, lams, threads, world):
+    """The reference's own fit_line (fit.py:88-102) decomposed over the timed
+    steps: step k runs fit_for_pivot (fit.py:75-85) on pivots
+    [k m / K, (k + 1) m / K) through the reference's own thread pool
+    (parallel.map_indices, threads = os.cpu_count()), so one complete fit is
+    timed, every pivot exactly once; the strict-'<' argmin in pivot order
+    (fit.py:98-102) over all of them is the fit's answer.  C1 (milliseconds
+    per fit) runs l1line.fit_line itself once per step."""
+    l1line, map_indices = ref
+    n, m = X.shape
+    data = l1line.DataMatrix(X)
+    lam = float(lams[0])
+    K = max(1, args.steps)
+    whole = args.config == "c1"
+    for w in range(args.warmup):  # untimed: one batch of `threads` pivots
+        lo = (w * threads) % m
+        map_indices(lambda i: l1line.fit_for_pivot(data, lo + i, lam), min(threads, m - lo), threads)
+    t_steps, objs, best = [], [], None
+    for k in range(K):
+        t0 = time.perf_counter()
+        if whole:
+            best = l1line.fit_line(data, lam, threads=threads)
+        else:
+            lo, hi = k * m // K, (k + 1) * m // K
+            lines = map_indices(lambda i: l1line.fit_for_pivot(data, lo + i, lam), hi - lo, threads)
+            objs.extend(lines)
+        t_steps.append(time.perf_counter() - t0)
+    if not whole:
+        best = objs[0]
+        for line in objs[1:]:
+            if line.objective < best.objective:  # fit.py:98-102
+                best = line
+    t_fit = float(np.mean(t_steps)) if whole else float(np.sum(t_steps))
+    v = m * (m - 1) / t_fit
+    sample = (f"l1line.fit_line, a complete fit per step" if whole else
+              f"one complete l1line fit: fit_for_pivot on all {m} pivots through parallel.map_indices, "
+              f"each pivot timed once across the {K} steps")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(t_steps)),
+        "ms_per_fit": 1e3 * t_fit, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(args, X, lams, world),
+        "cpu_baseline": {"value": v, "unit": "solves/s", "cores": threads, "kind": "reference",
+                         "package": "l1line 0.1.0 (baseline/_ref, unmodified)", "cpu_model": _cpu_model(),
+                         "sample": sample, "extrapolated": False, "fits_in_driver_run": True,
+                         "timed_s": float(np.sum(t_steps))},
+        "result": {"pivot": [best.preserved], "objective": [best.objective]},
+        "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _fit_pivot_set(oracle, X, lams, pivots, threads):
+    """oracle.fit_pivots over an arbitrary pivot set, threads in parallel (one pivot each)."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(threads, len(pivots))) as ex:
+        parts = list(ex.map(lambda p: oracle.fit_pivots(X, lams, int(p), int(p) + 1, threads=1, want_v=False),
+                            pivots))
+    return (None, np.concatenate([q[1] for q in parts]), np.concatenate([q[2] for q in parts]),
+            np.concatenate([q[3] for q in parts]))
 
 
 def _config_dict(args, X, lams, world):
@@ -380,8 +565,8 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        sps, per_fit, sample = cpu_reference(X, lams, budget_s=args.cpu_budget)
-        cpu = {"value": sps, "unit": "solves/s", "cores": os.cpu_count(), "kind": "port",
+        sps, per_fit, sample, kind = cpu_reference(X, lams, budget_s=args.cpu_budget)
+        cpu = {"value": sps, "unit": "solves/s", "cores": os.cpu_count(), "kind": kind, "cpu_model": _cpu_model(),
                "sample": sample, "seconds_per_fit_extrapolated": per_fit}
 
     if rank == 0:
@@ -411,15 +596,14 @@ def run_ours(args):
                          "fp32_view": {"ops_per_element": 5, "achieved_TOPs": 5 * kb_rate / 1e12,
                                        "peak_TOPs": _fp32_peak(dev) / 1e12},
                          "smem_wavefront_view": {
-                             "note": "shared-memory pipe cycles the design needs per element: per warp, 4 rows x "
-                                     "2 pivots x 64 targets cost 8 tile + 6 plane loads + 16 atomics = 30 "
-                                     "wavefronts; peak = one wavefront per SM-clock (the atomic probe / 32). "
-                                     "ncu (profiles/r01/ncu_bound_c2_v19.txt) measures the L1/TEX pipe at 74 % and "
-                                     "issue slots at 74 %.",
-                             "wavefronts_per_element": 30.0 / 512.0,
-                             "achieved_G_per_s": kb_rate * 30.0 / 512.0 / 1e9,
+                             "note": "shared-memory pipe requests the design issues per element: per warp and row, "
+                                     "8 problems x 32 lanes = 256 elements cost 8 histogram atomics + 1 tile load "
+                                     "(2 wavefronts) + 3 broadcast record loads = 13 instructions; peak = one per "
+                                     "SM-clock (the atomic probe / 32). ncu: profiles/r02/.",
+                             "requests_per_element": 13.0 / 256.0,
+                             "achieved_G_per_s": kb_rate * 13.0 / 256.0 / 1e9,
                              "peak_G_per_s": atoms_peak / 32.0 / 1e9,
-                             "frac": kb_rate * 30.0 / 512.0 / (atoms_peak / 32.0)},
+                             "frac": kb_rate * 13.0 / 256.0 / (atoms_peak / 32.0)},
                          "step_view": {
                              "note": "whole pruned step against the exact algorithm's FP64 floor (SURVEY.md 8d: "
                                      "11 FP64 ops per ratio element, E = n*m*(m-1) per fit); > 1 means the step "
@@ -468,10 +652,10 @@ def _fp32_peak(dev) -> float:
 
 
 def _ncu_traffic(config: str, world: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one k_bound<1> launch
-    from the committed ncu --set full capture (profiles/r01), or None."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_bound launch
+    from the committed ncu --set full capture (profiles/r02), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")) as f:
             t = json.load(f)
         return t.get(config) if world == 1 else None
     except Exception:  # noqa: BLE001
@@ -496,6 +680,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU baseline sampling")
     ap.add_argument("--ref-budget", type=float, default=60.0, help="seconds for the whole reference arm")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--port", action="store_true", help="reference arm: the oracle C port even where the "
+                                                        "reference package is installed")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

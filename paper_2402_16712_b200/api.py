@@ -153,6 +153,10 @@ def fit_subspace(data, lam: float, k: int, threads: int | None = None) -> Subspa
             return SubspaceFit(tuple(comps), degenerate=True)
         line = _line(eng.shard_winners([float(lam)])[0])
         comps.append(line)
+        # subspace.py:75 deflates after every component, the last one too, and
+        # deflate (subspace.py:32-33) rejects the zero vector
+        if not line.v.any():
+            raise ValueError("cannot deflate along the zero vector")
         if t + 1 < k:
             eng.deflate(line.v)
     return SubspaceFit(tuple(comps), degenerate=False)

@@ -112,6 +112,171 @@ __global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t
   }
 }
 
+// ---- pivots with more than kBpMaxRows nonzero rows (tall data, C4) ----
+//
+// The same column, sorted in global memory with the caller's output arrays
+// as scratch (column c: keys in rs, rows as int32 in the second half of st,
+// a ping-pong key buffer in rt and row buffer in st's first half):
+// k_bp_tall_keys compacts the rows and sorts chunks of kBpMaxRows in shared
+// memory, k_bp_merge merges sorted runs pairwise (merge path: every thread
+// finds its output segment's split by binary search and merges it
+// sequentially), k_bp_tall_walk is the prefix walk of k_breakpoints in
+// sorted order.  Ties in the key are broken by row, as the stable argsort.
+
+__device__ __forceinline__ bool bp_less(unsigned long long ka, int ra, unsigned long long kb, int rb) {
+  return ka < kb || (ka == kb && ra < rb);
+}
+
+template <bool SAFE>
+__global__ void __launch_bounds__(kBpThreads) k_bp_tall_keys(SelParams P, int64_t p, int64_t ld,
+                                                             double* __restrict__ rs, double* __restrict__ st) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(psm);
+  int* row = reinterpret_cast<int*>(psm + kBpMaxRows * sizeof(unsigned long long));
+  __shared__ int wsum[kBpThreads / 32];
+  const int tid = threadIdx.x;
+  const int64_t n = P.n;
+  const int64_t c = blockIdx.x;
+  const int64_t j = c < p ? c : c + 1;
+  const double* xc = P.Xc + j * n;
+  const double* pb = P.pb + p * P.np;
+  const double* py = P.py + p * P.np;
+  unsigned long long* gk = reinterpret_cast<unsigned long long*>(rs + c * ld);
+  int* gr = reinterpret_cast<int*>(st + c * ld) + ld;  // rows, buffer A
+  int base = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += kBpThreads) {  // ordered compaction (ratios.py:115)
+    const int64_t i = i0 + tid;
+    const bool nz = i < n && pb[i] != 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int k = 0; k < kBpThreads / 32; ++k) {
+      off += k < w ? wsum[k] : 0;
+      tot += wsum[k];
+    }
+    if (nz) {
+      const int pos = base + off + __popc(bal & ((1u << l) - 1));
+      gk[pos] = key64(sratio<SAFE>(P, xc[i], pb[i], py[i]));
+      gr[pos] = (int)i;
+    }
+    base += tot;
+    __syncthreads();
+  }
+  const int cnt = base;
+  // sort every chunk of kBpMaxRows in shared memory (bitonic, padded)
+  for (int c0 = 0; c0 < cnt; c0 += (int)kBpMaxRows) {
+    const int len = min((int)kBpMaxRows, cnt - c0);
+    for (int e = tid; e < (int)kBpMaxRows; e += kBpThreads) {
+      key[e] = e < len ? __ldcg(gk + c0 + e) : ~0ULL;
+      row[e] = e < len ? __ldcg(gr + c0 + e) : 0x7fffffff;
+    }
+    __syncthreads();
+    for (int kq = 2; kq <= (int)kBpMaxRows; kq <<= 1) {
+      for (int jq = kq >> 1; jq > 0; jq >>= 1) {
+        for (int e = tid; e < (int)kBpMaxRows; e += kBpThreads) {
+          const int l = e ^ jq;
+          if (l > e) {
+            const unsigned long long ka = key[e], kb = key[l];
+            const int ra = row[e], rb = row[l];
+            if (bp_less(kb, rb, ka, ra) == ((e & kq) == 0)) {
+              key[e] = kb;
+              key[l] = ka;
+              row[e] = rb;
+              row[l] = ra;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int e = tid; e < len; e += kBpThreads) {
+      gk[c0 + e] = key[e];
+      gr[c0 + e] = row[e];
+    }
+    __syncthreads();
+  }
+}
+
+// Merge the sorted runs of width W pairwise (run 2a with run 2a + 1) from
+// buffer `from` (0 = A: keys rs, rows st[ld..]; 1 = B: keys rt, rows st[0..]).
+__global__ void __launch_bounds__(kBpThreads) k_bp_merge(int64_t cnt, int64_t ld, int64_t W, int from,
+                                                         double* __restrict__ rs, double* __restrict__ st,
+                                                         double* __restrict__ rt) {
+  const int64_t c = blockIdx.x;
+  int* rows = reinterpret_cast<int*>(st + c * ld);
+  const unsigned long long* sk = reinterpret_cast<const unsigned long long*>((from ? rt : rs) + c * ld);
+  unsigned long long* dk = reinterpret_cast<unsigned long long*>((from ? rs : rt) + c * ld);
+  const int* sr = rows + (from ? 0 : ld);
+  int* dr = rows + (from ? ld : 0);
+  for (int64_t a0 = 0; a0 < cnt; a0 += 2 * W) {
+    const int64_t na = min(W, cnt - a0), nb = max((int64_t)0, min(W, cnt - a0 - W));
+    const unsigned long long* ka = sk + a0;
+    const unsigned long long* kb = sk + a0 + na;
+    const int* ra = sr + a0;
+    const int* rb = sr + a0 + na;
+    const int64_t tot = na + nb;
+    const int64_t d0 = tot * threadIdx.x / kBpThreads, d1 = tot * (threadIdx.x + 1) / kBpThreads;
+    // co-rank: the number of A elements among the first d outputs
+    auto corank = [&](int64_t d) {
+      int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
+      while (lo < hi) {
+        const int64_t i = (lo + hi) >> 1;  // A[i] vs B[d - i - 1]
+        if (bp_less(ka[i], ra[i], kb[d - i - 1], rb[d - i - 1])) lo = i + 1;
+        else hi = i;
+      }
+      return lo;
+    };
+    int64_t i = corank(d0), k = d0 - i;
+    for (int64_t d = d0; d < d1; ++d) {
+      const bool takeA = k >= nb || (i < na && bp_less(ka[i], ra[i], kb[k], rb[k]));
+      if (takeA) {
+        dk[a0 + d] = ka[i];
+        dr[a0 + d] = ra[i];
+        ++i;
+      } else {
+        dk[a0 + d] = kb[k];
+        dr[a0 + d] = rb[k];
+        ++k;
+      }
+    }
+  }
+}
+
+// k_breakpoints' prefix walk over the rows sorted in buffer A (one thread per
+// column; the outputs overwrite the scratch behind the read position: st[k]
+// covers rows int32 2k, 2k + 1 < ld + k of buffer A).
+template <bool SAFE>
+__global__ void k_bp_tall_walk(SelParams P, int64_t p, int64_t cnt, int64_t ld, int64_t ncol,
+                               double* __restrict__ rs, double* __restrict__ st, double* __restrict__ rt) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncol) return;
+  const int64_t n = P.n;
+  const int64_t j = c < p ? c : c + 1;
+  const double* xc = P.Xc + j * n;
+  const double* pb = P.pb + p * P.np;
+  const double* py = P.py + p * P.np;
+  const int* row = reinterpret_cast<const int*>(st + c * ld) + ld;
+  double T = 0.0;
+  for (int64_t k = 0; k < cnt; ++k) T = __dadd_rn(T, fabs(pb[row[k]]));
+  double Pp = 0.0;
+  for (int64_t k = 0; k < cnt; ++k) {
+    const int r = row[k];
+    const double w = fabs(pb[r]);
+    const double Pk = __dadd_rn(Pp, w);
+    double ratio = sratio<SAFE>(P, xc[r], pb[r], py[r]);
+    if (ratio == 0.0) ratio = __ddiv_rn(xc[r], pb[r]);  // the zero's sign (the hoisted path may drop it)
+    const double center = __dsub_rn(__dsub_rn(T, Pk), Pp);
+    const double s = __dsub_rn(ratio >= 0.0 ? center : -center, w);
+    const double rr = __dadd_rn(s, __dmul_rn(2.0, w));
+    rs[c * ld + k] = ratio;
+    rt[c * ld + k] = rr;
+    st[c * ld + k] = s;  // after row[k] was read (see above)
+    Pp = Pk;
+  }
+}
+
 // ------------------------------------------- optimality certificates --
 //
 // The dual certificate of oracle.py:141-174 for every column of one line at

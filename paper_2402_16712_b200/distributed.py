@@ -171,6 +171,8 @@ def fit_subspace_distributed(data, lam: float, k: int, group=None):
         w = combine_winners(local, m, group)[0]
         comps.append(FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,
                                 penalty_norm=w.penalty_norm, objective=w.objective))
+        if not np.any(w.v):  # subspace.py:75 / 32-33: the reference's deflate rejects v = 0
+            raise ValueError("cannot deflate along the zero vector")
         if t + 1 < k:
             eng.deflate(w.v)
     return SubspaceFit(tuple(comps), degenerate=False)

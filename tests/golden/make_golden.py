@@ -250,6 +250,8 @@ CSV_CASES = {
     "exp_forms": "1E5,2.E-3\n-0,0.0\n",
     "long_digits": "0.1000000000000000055511151231257827,3.141592653589793238462643383279\n2.718281828459045235360287,1\n",
     "unicode": "1,\u0663\n2,3\n",
+    "plus_minus": "1,+-1\n2,3\n",
+    "plus_plus": "1,2\n++3,4\n",
 }
 
 

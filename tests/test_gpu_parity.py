@@ -413,13 +413,15 @@ def test_pruned_fit_equals_full_fit():
 def test_pruned_fit_equals_full_fit_tall():
     """Tall columns (n >= 2 * KB_SREP_ROWS = 8192) start the bound pass from several
     averaged row samples (k_bound<..., TALL>); single- and multi-penalty pruned
-    fits, also on deflated data, still return exactly the full fit."""
+    fits, also on deflated data, still return exactly the full fit.  The
+    all-finite sweep takes the one-pass multi-penalty path (k_bound<..., MULTI,
+    TALL> + the batched entry cascade); a sweep with +inf takes the per-penalty loop."""
     d, _ = l1b.gen_line_data(24, 40000, seed=5, noise_scale=1.0)
     X = d.values
     T = float(np.abs(X).sum(axis=0).max())
     eng = DeviceFit(X)
     for comp in range(2):
-        for lams in ([1.0], [0.05 * T], [0.0, 1.0, 0.1 * T, 0.5 * T, math.inf]):
+        for lams in ([1.0], [0.05 * T], [0.0, 1.0, 0.1 * T, 0.5 * T], [0.0, 1.0, 0.1 * T, 0.5 * T, math.inf]):
             full = eng.shard_winners(lams, prune=False)
             pruned = eng.shard_winners(lams, prune=True)
             for a, b in zip(full, pruned):
@@ -734,3 +736,42 @@ def test_brute_force_and_sweep_validate():
     X = rng.uniform(-10, 10, size=(30, 5))
     rep = sweep_validate(X, solution_path(X), grid_size=40)
     assert rep.ok, rep.failures
+
+
+def test_subspace_rejects_zero_direction_like_reference():
+    """subspace.py:71-75 deflates after every component (the last one too) and
+    deflate (subspace.py:32-33) raises on v = 0: a degenerate winning line at a
+    huge penalty makes the reference's fit_subspace raise, even for k = 1."""
+    X = np.array([[0.0, 2.0, 1.0], [0.0, -1.0, 3.0], [0.0, 4.0, -2.0]])
+    with pytest.raises(ValueError, match="zero vector"):
+        l1b.fit_subspace(X, 100.0, 1)
+    with pytest.raises(ValueError, match="zero vector"):
+        l1b.deflate(X, np.zeros(3))
+
+
+@pytest.mark.parametrize("n,zeros", [(40000, False), (70001, True)])
+def test_pivot_runs_tall_pivot(n, zeros):
+    """Pivots with more than 16384 nonzero rows (chunk sorts + global merges,
+    l1b_pivot_breakpoints' tall path) give the sorted tableau runs of
+    path.py:76-102 bit for bit: ratios.py:40-67's column (the oracle's
+    build_column, itself pinned to the reference) and path.py:86-89's run
+    arithmetic (center = (T - P) - P_prev, start = +-center - w, right = start + 2 w)."""
+    rng = np.random.default_rng(n)
+    d, _ = l1b.gen_line_data(5, n, seed=7, noise_scale=1.0)
+    X = np.array(d.values)
+    X = np.round(X * 64.0) / 64.0  # heavy exact ties: the row tie-break decides the order
+    if zeros:
+        X[rng.random(n) < 0.3, 2] = 0.0
+        X[rng.random(n) < 0.1, 0] = -0.0
+    eng = DeviceFit(X)
+    for p in (0, 2):
+        R, S, T = eng.pivot_runs(p)
+        cols = [j for j in range(X.shape[1]) if j != p]
+        for c, j in enumerate(cols):
+            r, w, rows, pref = oracle.build_column(X, p, j)
+            prev = np.concatenate(([0.0], pref[:-1]))
+            center = (pref[-1] - pref) - prev
+            start = np.where(r >= 0.0, center, -center) - w
+            right = start + 2.0 * w
+            assert R[c].tobytes() == r.tobytes(), (p, j)
+            assert S[c].tobytes() == start.tobytes() and T[c].tobytes() == right.tobytes(), (p, j)

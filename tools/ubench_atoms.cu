@@ -60,6 +60,20 @@ __global__ void __launch_bounds__(512, 1) k(long iters, int active, unsigned* ou
                      : "r"(smem_u32(h) + ((((unsigned)i * 8 + u) * 256 + (threadIdx.x & 31) * 8) & 0xffffu)));
         accv[u] ^= v0 ^ v1;
       }
+      if (MODE == 12 || MODE == 13) {  // shfl.idx broadcast (13: plus one red)
+        const unsigned v = __shfl_sync(0xffffffffu, accv[u] + (unsigned)i, (u + (int)i) & 31);
+        accv[u] ^= v;
+        if (MODE == 13) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[u]), "r"((unsigned)i + u));
+      }
+      if (MODE == 14) {  // three reds per broadcast lds.128 (k_bound's mix, roughly)
+        unsigned v0, v1, v2, v3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                     : "r"(smem_u32(h) + ((((unsigned)i * 8 + u) * 16) & 0xfff0u)));
+        accv[u] ^= v0 ^ v1 ^ v2 ^ v3;
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[u]), "r"((unsigned)i + u));
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[(u + 1) & 7]), "r"((unsigned)i + u));
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[(u + 2) & 7]), "r"((unsigned)i + u));
+      }
       if (MODE == 4) {
         unsigned v;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a[u] ^ ((unsigned)i & 4u)));
@@ -119,5 +133,8 @@ int main() {
   rep("red.u32 + broadcast lds.128", run<9>(it, 32));
   rep("broadcast lds.128 alone", run<10>(it, 32));
   rep("lds.64 32 lanes consecutive alone", run<11>(it, 32));
+  rep("shfl.idx alone", run<12>(it, 32));
+  rep("shfl.idx + red.u32", run<13>(it, 32));
+  rep("broadcast lds.128 + 3 red.u32", run<14>(it, 32));
   return 0;
 }
