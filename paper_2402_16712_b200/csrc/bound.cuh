@@ -429,6 +429,48 @@ __device__ __forceinline__ void sample_bracket(const SelParams& P, int64_t p, in
     sample_bracket1(P, p, tbase, lane, Tq, unit, delta, lo, hi, cen, smin, smax, lam_lo, lam_hi, 0, 1);
 }
 
+// Steering (P.steer = s): the histogram of a 1-in-s chunk sample of the rows
+// locates where the column's lambda-shifted weighted median lies; the next
+// pass brackets that location widened by the sample's error, so its 62 bins
+// are several times narrower than a 32-row sample's bracket allows (tall
+// data, where one pass cannot prune deflated components).  Only steers: any
+// range gives rigorous bounds in the pass that uses it.
+//   Sample weight T_s (exact sum of the sampled u32 weights), penalty scaled
+//   to the sample, lam_s = lam T_s / T; the crossing's cumulative weight lies
+//   in [(T_s - lam_s) / 2, (T_s + lam_s) / 2] (both signs of v, and the dead
+//   zone between), widened by delta = 3 T_s / sqrt(n_s) for the sampling
+//   error of a weighted quantile (n_s = nnz / s sampled rows).
+__device__ __forceinline__ float2 steer_range(const Prefix& H, float lo, float hi, double lam, double T, long long nnz,
+                                              int s, double q, float smin, float smax) {
+  const unsigned tot = H.cu(kNB - 1);
+  const float span = hi - lo;
+  if (tot == 0u) return make_float2(lo, hi);
+  const double Ts = q * (double)tot;
+  const double ns = fmax(1.0, (double)nnz / (double)s);
+  const double lam_s = T > 0.0 ? lam * Ts / T : 0.0;
+  const double delta = 3.0 * Ts / sqrt(ns);
+  const double glo = 0.5 * (Ts - lam_s) - delta, ghi = 0.5 * (Ts + lam_s) + delta;
+  // smallest k with C_k >= g: the crossing lies below edge k (slot k)
+  auto first_ge = [&](double g) {
+    int a = -1, b = kNB - 1;  // C at slot kNB - 1 is the total
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (q * (double)H.cu(mid) >= g) b = mid;
+      else a = mid;
+    }
+    return b;
+  };
+  const int ka = first_ge(glo), kb = first_ge(ghi);
+  const double w = ((double)hi - (double)lo) / (double)kNI;
+  float a = ka <= 0 ? fminf(smin, lo) - 2.f * span : (float)((double)lo + (double)(ka - 1) * w);
+  float b = kb >= kNI + 1 ? fmaxf(smax, hi) + 2.f * span : (float)((double)lo + (double)kb * w);
+  const float mg = 0.02f * (b - a);
+  a -= mg;
+  b += mg;
+  if (!(b > a)) b = a + fmaxf(fabsf(a), 1e-30f) * 1e-6f;
+  return make_float2(a, b);
+}
+
 // One bounding pass per (pivot, target) problem.  CONT = false: the range
 // comes from a row sample (sample_bracket, half-width P.delta ranks).
 // CONT = true (refinement for the pivots an earlier pass could not rule out):
@@ -486,13 +528,15 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   };
   const int64_t nall = (n + kBRows - 1) / kBRows;
   const int64_t cb = SPLIT ? nall * blockIdx.z / gridDim.z : 0;  // this CTA's chunks [cb, cb + nch)
-  const int64_t nch = SPLIT ? nall * (blockIdx.z + 1) / gridDim.z - cb : nall;
+  // a steering pass (P.steer = s > 1, never SPLIT) takes every s-th chunk
+  const int64_t cstep = !SPLIT && P.steer > 1 ? P.steer : 1;
+  const int64_t nch = SPLIT ? nall * (blockIdx.z + 1) / gridDim.z - cb : (nall + cstep - 1) / cstep;
   // stage refill: local chunk c (global cb + c) goes to stage c % kBStages
   // (no proxy fence in the loop: the ring is only ever read by generic
   // loads there, and a fence would drain the issuing warp's histogram atomics)
   auto issue = [&](int64_t c) {
     const int st = (int)(c % kBStages);
-    const int64_t i0 = (cb + c) * kBRows;
+    const int64_t i0 = (cb + c * cstep) * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
     mbar_expect_tx(&full[st], (unsigned)(kBTile + kBPlane));
     bulk_g2s(base, P.Xq + ((int64_t)blockIdx.x * np + i0) * kBTgt, kBTile, &full[st]);
@@ -689,6 +733,16 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   double T, u;
   meta(pv, okk, dg, T, u);
   const bool live = okk && qj < m && !dg && qj != pv;
+  if (!SPLIT && !MULTI && P.steer > 1) {  // steering pass: the next range only
+    if (okk && qj < m) {
+      Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
+      H.build();
+      P.NEXTw[qk * m + qj] = live ? steer_range(H, tlo, thi, lam_of(P, qk), T * u, P.nnz[pv], P.steer,
+                                                ldexp(u, 21), sbr[3][tid], sbr[4][tid])
+                                  : make_float2(tlo, thi);
+    }
+    return;
+  }
   if (MULTI) {
     Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
     H.build();  // once for every penalty

@@ -15,6 +15,8 @@ constexpr double kRescoreRtol = 1e-8;   // engine.RESCORE_RTOL
 constexpr double kRescoreAtol = 1e-13;  // engine.RESCORE_ATOL (times n m max|x|)
 constexpr double kPruneRtol = 1e-9;     // engine.PRUNE_RTOL
 constexpr int kRefineMin = 2, kRefinePasses = 3;
+constexpr int64_t kSteerRows = 32768;  // rows from which the first pass is steered by a row sample
+constexpr int kSteerStride = 8;        // the steering sample: every 8th 64-row chunk
 
 // NumPy's pairwise_sum_DOUBLE for a contiguous array (loops_utils.h.src):
 // n < 8 sequential, n <= 128 eight strided accumulators, else split at n/2
@@ -84,8 +86,12 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
   if (do_prune) {
     // lean: per-pivot bound sums and next ranges only (the continuing passes
     // over the survivors write their seeds and column bounds)
+    // tall columns: a steering pass over a row sample narrows the first full
+    // pass's brackets (deflated components of tall data prune only then)
+    int steer = n >= kSteerRows ? kSteerStride : 0;
+    if (const char* e = getenv("L1B200_STEER")) steer = atoi(e);  // tuning knob: chunk stride, 0 = off
     st = fit_impl(d_X, n, m, &lam, 1, p_begin, p_stride, nullptr, npiv, true, nullptr, nullptr, nullptr, nullptr,
-                  d_lb, d_ub, d_ws, ws_bytes, stream, 1, nullptr, 0, nullptr, nullptr, nullptr, /*lean=*/true);
+                  d_lb, d_ub, d_ws, ws_bytes, stream, 1, nullptr, 0, nullptr, nullptr, nullptr, /*lean=*/true, steer);
     if (st != L1B_OK) return st;
     if (cudaMemcpyAsync(lb.data(), d_lb, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaMemcpyAsync(ub.data(), d_ub, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())

@@ -95,7 +95,8 @@ struct SelParams {
   unsigned long long* LBq;  // k_bound: per (penalty, pivot) column-bound sums, fixed point 2^-fxk ([nlam][npiv])
   unsigned long long* UBq;
   const int* fxk;        // fixed-point exponent (k_fxscale)
-  int lean;              // k_bound: per-pivot sums only (no per-problem LB / UB / BRK / NEXT records)
+  int lean;              // k_bound: per-pivot sums and next ranges only (no LB / UB / BRK records)
+  int steer;             // k_bound: a steering pass over every steer-th row chunk (next ranges only)
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {
