@@ -92,10 +92,24 @@ int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_
  * d_right[c*ld + k] = start + 2 w_k, k < *h_nrows (the pivot's nonzero
  * rows), bit-identical to the reference's NumPy arithmetic.  With all three
  * outputs NULL it only reports *h_nrows (0: zero pivot column, the
- * reference's EmptyPivotError).  Needs l1b_prepare; *h_nrows <= 16384. */
+ * reference's EmptyPivotError).  Needs l1b_prepare.  Up to 16384 nonzero
+ * rows a column is sorted in shared memory; beyond, the three output arrays
+ * double as scratch for chunk sorts and global merges (same results). */
 int l1b_pivot_breakpoints(const double* d_X, int64_t n, int64_t m, int64_t pivot, int64_t* h_nrows,
                           double* d_ratios, double* d_start, double* d_right, int64_t ld, void* d_ws,
                           size_t ws_bytes, void* stream);
+
+/* pivot_tableau / build_column (ratios.py:40-67, 109-135) on the device:
+ * for target column `target` (or, target < 0, every target j != pivot in
+ * ascending order, output column c), the column in stable (ratio, row)
+ * order: d_ratios[c*ld + k] = fl(x_ij / x_ip), d_weights = |x_ip|,
+ * d_prefix = np.cumsum's sequential inclusive prefix, d_rows = source row,
+ * k < *h_nrows (the pivot's nonzero rows), bit-identical to the reference.
+ * Outputs NULL: size query only (*h_nrows = 0 is the EmptyPivotError case).
+ * Replaces the NumPy sort of ratios.py:55,121. */
+int l1b_pivot_tableau(const double* d_X, int64_t n, int64_t m, int64_t pivot, int64_t target, int64_t* h_nrows,
+                      double* d_ratios, double* d_weights, double* d_prefix, int64_t* d_rows, int64_t ld,
+                      void* d_ws, size_t ws_bytes, void* stream);
 
 /* brute_force_column (oracle.py:39-58) for every target column of one pivot
  * (targets j != pivot ascending): the objective at every kink candidate

@@ -8,7 +8,8 @@ GPU (types, data generation); the first fit loads ``csrc/libl1b200.so`` and
 requires a CUDA device -- there is no CPU fallback.
 """
 
-from .core import DataMatrix, EmptyPivotError, FittedLine, PathSegment, SolutionPath, SubspaceFit
+from .core import (DataMatrix, DualCertificate, EmptyPivotError, FittedLine, PathSegment, RatioColumn, SolutionPath,
+                   SubspaceFit)
 from .datagen import gen_line_data, gen_outlier_data, laplace
 
 __version__ = "0.1.0"
@@ -20,9 +21,11 @@ _PATH = ("pivot_breakpoints", "major_breakpoints", "PivotBreakpoints", "PivotSol
 _CERT = ("certify_line", "check_line", "LineCertificate", "OptimalityRefuted")
 _IO = ("read_matrix", "write_matrix", "CsvParseError", "write_path", "read_path", "write_sweep")
 _VALIDATE = ("brute_force_column", "brute_force_pivot", "brute_force_line", "sweep_validate", "SweepReport")
+_TABLEAU = ("build_column", "pivot_tableau", "PivotTableau", "window_bounds", "solve_column", "dual_certificate")
 
-__all__ = ["DataMatrix", "EmptyPivotError", "FittedLine", "PathSegment", "SolutionPath", "SubspaceFit", "gen_line_data",
-           "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO, *_VALIDATE, "__version__"]
+__all__ = ["DataMatrix", "DualCertificate", "EmptyPivotError", "FittedLine", "PathSegment", "RatioColumn", "SolutionPath",
+           "SubspaceFit", "gen_line_data", "gen_outlier_data", "laplace", "use_gpu", *_API, *_PATH, *_CERT, *_IO,
+           *_VALIDATE, *_TABLEAU, "__version__"]
 
 
 def __getattr__(name):
@@ -42,6 +45,9 @@ def __getattr__(name):
     if name in _VALIDATE:
         from . import validate
         return getattr(validate, name)
+    if name in _TABLEAU:
+        from . import tableau
+        return getattr(tableau, name)
     if name == "use_gpu":
         from .integration import use_gpu
         return use_gpu

@@ -39,6 +39,7 @@ ABI_SYMBOLS = (
     "l1b_bound_pivot_list_continue",
     "l1b_bound_pivots_multi",
     "l1b_pivot_breakpoints",
+    "l1b_pivot_tableau",
     "l1b_certify_columns",
     "l1b_bound_entries",
     "l1b_fit_entries_seeded",
@@ -134,6 +135,9 @@ def load() -> ctypes.CDLL:
     lib.l1b_bound_pivots_multi.restype = ctypes.c_int
     lib.l1b_bound_pivots_multi.argtypes = [_vp, _i64, _i64, _vp, ctypes.c_int32, _i64, _i64, _i64, _vp, _vp, _vp,
                                            _vp, _sz, _vp]
+    lib.l1b_pivot_tableau.restype = ctypes.c_int
+    lib.l1b_pivot_tableau.argtypes = [_vp, _i64, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int64), _vp, _vp, _vp, _vp,
+                                      _i64, _vp, _sz, _vp]
     lib.l1b_pivot_breakpoints.restype = ctypes.c_int
     lib.l1b_pivot_breakpoints.argtypes = [_vp, _i64, _i64, _i64, ctypes.POINTER(ctypes.c_int64), _vp, _vp, _vp, _i64,
                                           _vp, _sz, _vp]

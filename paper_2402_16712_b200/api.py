@@ -67,6 +67,35 @@ def _as_data(data) -> DataMatrix:
                       column_names=getattr(data, "column_names", None))
 
 
+# Device replicas of read-only inputs, reused across calls (a caller looping
+# fit_for_pivot over every pivot uploads X once, not m times).  Keyed by the
+# identity of the caller's read-only values array (DataMatrix.values here and
+# in the reference, core.py:67); writable arrays are never cached.  The two
+# most recently used matrices stay resident.
+_ENGINES: list = []
+_ENGINE_SLOTS = 2
+
+
+def _engine(data, d: DataMatrix) -> DeviceFit:
+    """A full-capacity DeviceFit for d (cached when its values are read-only)."""
+    import weakref
+
+    import torch
+    src = getattr(data, "values", data)
+    if not (isinstance(src, np.ndarray) and not src.flags.writeable and src.dtype == np.float64
+            and src.flags.c_contiguous):
+        return DeviceFit(d.values)
+    dev = torch.cuda.current_device()
+    for i, (ref, edev, eng) in enumerate(_ENGINES):
+        if ref() is src and edev == dev:
+            _ENGINES.insert(0, _ENGINES.pop(i))
+            return eng
+    eng = DeviceFit(d.values)
+    _ENGINES.insert(0, (weakref.ref(src), dev, eng))
+    del _ENGINES[_ENGINE_SLOTS:]
+    return eng
+
+
 def _line(w) -> FittedLine:
     return FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,
                       penalty_norm=w.penalty_norm, objective=w.objective)
@@ -80,7 +109,7 @@ def fit_lines(data, lams, threads: int | None = None) -> list[FittedLine]:
     lams = [_check_lam(x) for x in np.atleast_1d(np.asarray(lams, dtype=np.float64))]
     resolve_threads(threads)
     d = _as_data(data)
-    eng = DeviceFit(d.values)
+    eng = _engine(data, d)
     return [_line(w) for w in eng.shard_winners(lams)]
 
 
@@ -96,7 +125,7 @@ def fit_for_pivot(data, pivot: int, lam: float) -> FittedLine:
     pivot = int(pivot)
     if not 0 <= pivot < d.m:
         raise IndexError(f"pivot column {pivot} out of range")
-    eng = DeviceFit(d.values, max_pivots=1)
+    eng = _engine(data, d)
     return _line(eng.shard_winners([lam], p_begin=pivot, p_stride=1, npiv=1)[0])
 
 
@@ -120,7 +149,7 @@ def residual_error(data, v, preserved: int) -> float:
     if v.shape != (d.m,):
         raise ValueError(f"v has shape {v.shape}, expected ({d.m},)")
     import torch
-    eng = DeviceFit(d.values, max_pivots=1)
+    eng = _engine(data, d)
     return eng.residual_exact(torch.from_numpy(np.ascontiguousarray(v)).to(eng.device), int(preserved))
 
 

@@ -21,8 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .api import _as_data
-from .engine import DeviceFit
+from .api import _as_data, _engine
 
 __all__ = ["OptimalityRefuted", "LineCertificate", "certify_line", "check_line"]
 
@@ -63,7 +62,7 @@ def certify_line(data, line, lam: float | None = None, tol: float = 1e-9) -> Lin
     if not np.any(colp):  # degenerate pivot: the line must be the zero line (fit.py:66-72)
         bad = tuple(int(j) for j in np.nonzero(v)[0])
         return LineCertificate(p, lam, np.full(d.m, np.inf), np.zeros(d.m), bad)
-    eng = DeviceFit(d.values, max_pivots=1)
+    eng = _engine(data, d)
     with torch.cuda.device(eng.device):
         vd = torch.from_numpy(v).to(eng.device)
         sl = torch.empty(d.m, dtype=torch.float64, device=eng.device)

@@ -16,18 +16,40 @@
 constexpr int kBpThreads = 1024;
 constexpr int64_t kBpMaxRows = 16384;  // nonzero rows of the pivot a CTA can sort in shared memory
 
+// TAB: the tableau column itself (pivot_tableau, ratios.py:109-135) instead
+// of the runs: rs = sorted ratios, st = weights, rt = inclusive prefix
+// (np.cumsum), rows = source rows.  Columns c0 + blockIdx.x of the pivot's
+// targets (j != p), written at output column blockIdx.x.
+__device__ __forceinline__ void bp_emit(bool tab, double ratio, double w, double Pk, double T, double Pp, int r,
+                                        int64_t o, double* rs, double* st, double* rt, int64_t* rows) {
+  if (tab) {
+    rs[o] = ratio;
+    st[o] = w;
+    rt[o] = Pk;
+    rows[o] = r;
+  } else {
+    const double center = __dsub_rn(__dsub_rn(T, Pk), Pp);
+    const double s = __dsub_rn(ratio >= 0.0 ? center : -center, w);
+    rs[o] = ratio;
+    rt[o] = __dadd_rn(s, __dmul_rn(2.0, w));
+    st[o] = s;  // last: the tall walk's rows share st's storage (see k_bp_tall_walk)
+  }
+}
+
 template <bool SAFE>
 __global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t p, int64_t np2, int64_t ld,
                                                             double* __restrict__ rs, double* __restrict__ st,
-                                                            double* __restrict__ rt) {
+                                                            double* __restrict__ rt, int64_t c0, int tab,
+                                                            int64_t* __restrict__ rows_out) {
   extern __shared__ __align__(16) unsigned char psm[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(psm);
   int* row = reinterpret_cast<int*>(psm + np2 * sizeof(unsigned long long));
   __shared__ int cnt_s;
   const int tid = threadIdx.x;
   const int64_t n = P.n, m = P.m;
-  const int64_t c = blockIdx.x;           // target column index among j != p
-  const int64_t j = c < p ? c : c + 1;
+  const int64_t c = blockIdx.x;           // output column
+  const int64_t cj = c0 + c;              // target column index among j != p
+  const int64_t j = cj < p ? cj : cj + 1;
   const double* xc = P.Xc + j * n;
   const double* pb = P.pb + p * P.np;
   const double* py = P.py + p * P.np;
@@ -101,12 +123,7 @@ __global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t
       const double Pk = __dadd_rn(Pp, w);
       double ratio = sratio<SAFE>(P, xc[r], pb[r], py[r]);
       if (ratio == 0.0) ratio = __ddiv_rn(xc[r], pb[r]);  // the zero's sign (the hoisted path may drop it)
-      const double center = __dsub_rn(__dsub_rn(T, Pk), Pp);
-      const double s = __dsub_rn(ratio >= 0.0 ? center : -center, w);
-      const double rr = __dadd_rn(s, __dmul_rn(2.0, w));
-      rs[c * ld + k] = ratio;
-      st[c * ld + k] = s;
-      rt[c * ld + k] = rr;
+      bp_emit(tab, ratio, w, Pk, T, Pp, r, c * ld + k, rs, st, rt, rows_out);
       Pp = Pk;
     }
   }
@@ -129,15 +146,16 @@ __device__ __forceinline__ bool bp_less(unsigned long long ka, int ra, unsigned 
 
 template <bool SAFE>
 __global__ void __launch_bounds__(kBpThreads) k_bp_tall_keys(SelParams P, int64_t p, int64_t ld,
-                                                             double* __restrict__ rs, double* __restrict__ st) {
+                                                             double* __restrict__ rs, double* __restrict__ st,
+                                                             int64_t c0) {
   extern __shared__ __align__(16) unsigned char psm[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(psm);
   int* row = reinterpret_cast<int*>(psm + kBpMaxRows * sizeof(unsigned long long));
   __shared__ int wsum[kBpThreads / 32];
   const int tid = threadIdx.x;
   const int64_t n = P.n;
-  const int64_t c = blockIdx.x;
-  const int64_t j = c < p ? c : c + 1;
+  const int64_t c = blockIdx.x, cj = c0 + c;
+  const int64_t j = cj < p ? cj : cj + 1;
   const double* xc = P.Xc + j * n;
   const double* pb = P.pb + p * P.np;
   const double* py = P.py + p * P.np;
@@ -249,11 +267,13 @@ __global__ void __launch_bounds__(kBpThreads) k_bp_merge(int64_t cnt, int64_t ld
 // covers rows int32 2k, 2k + 1 < ld + k of buffer A).
 template <bool SAFE>
 __global__ void k_bp_tall_walk(SelParams P, int64_t p, int64_t cnt, int64_t ld, int64_t ncol,
-                               double* __restrict__ rs, double* __restrict__ st, double* __restrict__ rt) {
+                               double* __restrict__ rs, double* __restrict__ st, double* __restrict__ rt,
+                               int64_t c0, int tab, int64_t* __restrict__ rows_out) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncol) return;
   const int64_t n = P.n;
-  const int64_t j = c < p ? c : c + 1;
+  const int64_t cj = c0 + c;
+  const int64_t j = cj < p ? cj : cj + 1;
   const double* xc = P.Xc + j * n;
   const double* pb = P.pb + p * P.np;
   const double* py = P.py + p * P.np;
@@ -267,12 +287,7 @@ __global__ void k_bp_tall_walk(SelParams P, int64_t p, int64_t cnt, int64_t ld, 
     const double Pk = __dadd_rn(Pp, w);
     double ratio = sratio<SAFE>(P, xc[r], pb[r], py[r]);
     if (ratio == 0.0) ratio = __ddiv_rn(xc[r], pb[r]);  // the zero's sign (the hoisted path may drop it)
-    const double center = __dsub_rn(__dsub_rn(T, Pk), Pp);
-    const double s = __dsub_rn(ratio >= 0.0 ? center : -center, w);
-    const double rr = __dadd_rn(s, __dmul_rn(2.0, w));
-    rs[c * ld + k] = ratio;
-    rt[c * ld + k] = rr;
-    st[c * ld + k] = s;  // after row[k] was read (see above)
+    bp_emit(tab, ratio, w, Pk, T, Pp, r, c * ld + k, rs, st, rt, rows_out);  // st[k] after row[k] was read
     Pp = Pk;
   }
 }

@@ -271,6 +271,29 @@ class DeviceFit:
             h = out.cpu().numpy()
         return h[0], h[1], h[2]
 
+    def tableau(self, pivot: int, target: int = -1):
+        """Sorted tableau columns of one pivot (l1b_pivot_tableau, ratios.py:40-67 / 109-135):
+        ratios, weights, inclusive prefix [c][k] (f64) and source rows [c][k] (i64) for
+        target ``target`` (c = 0) or every target j != pivot; None for a zero pivot column."""
+        nr = ctypes.c_int64()
+        ncol = self.m - 1 if target < 0 else 1
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.l1b_pivot_tableau(self.X.data_ptr(), self.n, self.m, int(pivot), int(target),
+                                                  ctypes.byref(nr), None, None, None, None, 0, self.ws.data_ptr(),
+                                                  self.ws.numel(), self._s), "l1b_pivot_tableau")
+            k = int(nr.value)
+            if k == 0:
+                return None
+            out = torch.empty((3, ncol, k), dtype=torch.float64, device=self.device)
+            rows = torch.empty((ncol, k), dtype=torch.int64, device=self.device)
+            _lib.check(self.lib.l1b_pivot_tableau(self.X.data_ptr(), self.n, self.m, int(pivot), int(target),
+                                                  ctypes.byref(nr), out[0].data_ptr(), out[1].data_ptr(),
+                                                  out[2].data_ptr(), rows.data_ptr(), k, self.ws.data_ptr(),
+                                                  self.ws.numel(), self._s), "l1b_pivot_tableau")
+            h = out.cpu().numpy()
+            r = rows.cpu().numpy()
+        return h[0], h[1], h[2], r
+
     def bound_entries(self, lams, pivots, from_pos=None, from_count: int = 0, from_ranges=None):
         """One bounding pass per (pivot, penalty) entry (l1b_bound_entries); with
         from_pos, continuing from those entries of the last bound call (or of

@@ -18,8 +18,9 @@ _PATCHED = {}
 
 
 def use_gpu(module: str = "l1line") -> None:
-    """Patch ``l1line`` in place so fit_line / fit_for_pivot / fit_subspace and the
-    breakpoint maps (pivot_breakpoints / major_breakpoints, so solution_path too) use the GPU."""
+    """Patch ``l1line`` in place so fit_line / fit_for_pivot / fit_subspace, the sorted
+    tableau (build_column / pivot_tableau) and the breakpoint maps (pivot_breakpoints /
+    major_breakpoints, so solution_path too) use the GPU."""
     from . import api
 
     l1 = importlib.import_module(module)
@@ -78,7 +79,25 @@ def use_gpu(module: str = "l1line") -> None:
         from . import path
         return _conv_path(path.solution_path(data, threads))
 
+    def build_column(data, pivot, target):
+        # the device-sorted column as the reference's own RatioColumn
+        from . import tableau
+        c = tableau.build_column(data, pivot, target)
+        return ref_core.RatioColumn(pivot=c.pivot, target=c.target, ratios=c.ratios, weights=c.weights,
+                                    source_rows=c.source_rows, prefix_weights=c.prefix_weights,
+                                    total_weight=c.total_weight)
+
+    def pivot_tableau(data, pivot):
+        from . import tableau
+        rr = importlib.import_module(f"{module}.ratios")
+        t = tableau.pivot_tableau(data, pivot)
+        return rr.PivotTableau(pivot=t.pivot, targets=t.targets, ratios=t.ratios, weights=t.weights,
+                               source_rows=t.source_rows, prefix=t.prefix, prefix_prev=t.prefix_prev,
+                               totals=t.totals)
+
     targets = {
+        "build_column": build_column,
+        "pivot_tableau": pivot_tableau,
         "merge_path": merge_path,
         "solution_path": solution_path,
         "read_matrix": read_matrix,
@@ -88,7 +107,7 @@ def use_gpu(module: str = "l1line") -> None:
         "pivot_breakpoints": pivot_breakpoints,
         "major_breakpoints": major_breakpoints,
     }
-    for modname in ("", ".fit", ".subspace", ".oracle", ".cli", ".path", ".io"):
+    for modname in ("", ".ratios", ".fit", ".subspace", ".oracle", ".cli", ".path", ".io"):
         try:
             mod = importlib.import_module(module + modname)
         except ImportError:

@@ -28,7 +28,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .api import _as_data, resolve_threads
+from .api import _as_data, _engine, resolve_threads
 from .core import DataMatrix, EmptyPivotError, FittedLine, PathSegment, SolutionPath
 from .engine import DeviceFit
 
@@ -121,7 +121,7 @@ def pivot_breakpoints(data, pivot: int) -> PivotBreakpoints:
     d = _as_data(data)
     if not 0 <= pivot < d.m:
         raise IndexError(f"pivot column {pivot} out of range")
-    return _pivot_maps(DeviceFit(d.values, max_pivots=1), int(pivot))
+    return _pivot_maps(_engine(data, d), int(pivot))
 
 
 @dataclass(frozen=True)
@@ -148,7 +148,7 @@ def major_breakpoints(data, threads: int | None = None) -> tuple[np.ndarray, Piv
     the ascending deduplicated grid (starting at 0) and the per-pivot maps."""
     resolve_threads(threads)
     d = _as_data(data)
-    eng = DeviceFit(d.values, max_pivots=1)  # K0 once; one device pass per pivot
+    eng = _engine(data, d)  # K0 once; one device pass per pivot
     pivots: dict[int, PivotBreakpoints] = {}
     degenerate = []
     weights = [np.zeros(1)]  # the grid always starts at 0

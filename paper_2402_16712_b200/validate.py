@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .api import _as_data, _check_lam, fit_lines
+from .api import _as_data, _check_lam, _engine, fit_lines
 from .core import EmptyPivotError, FittedLine
 from .engine import DeviceFit
 
@@ -41,7 +41,7 @@ def brute_force_column(data, pivot: int, target: int, lam: float) -> tuple[float
     d = _as_data(data)
     if not np.any(d.values[:, pivot]):
         raise EmptyPivotError(f"column {pivot} is identically zero")
-    t, f = _columns(DeviceFit(d.values, max_pivots=1), pivot, lam)
+    t, f = _columns(_engine(data, d), pivot, lam)
     c = target if target < pivot else target - 1
     return float(t[c]), float(f[c])
 
@@ -61,13 +61,13 @@ def _pivot_line(eng: DeviceFit, d, pivot: int, lam: float) -> FittedLine:
 def brute_force_pivot(data, pivot: int, lam: float) -> FittedLine:
     """One pivot's line, column by column by brute force (oracle.py:61-71)."""
     d = _as_data(data)
-    return _pivot_line(DeviceFit(d.values, max_pivots=1), d, int(pivot), float(lam))
+    return _pivot_line(_engine(data, d), d, int(pivot), float(lam))
 
 
 def brute_force_line(data, lam: float) -> FittedLine:
     """Minimum over pivots of the brute-force lines (oracle.py:74-81)."""
     d = _as_data(data)
-    eng = DeviceFit(d.values, max_pivots=1)
+    eng = _engine(data, d)
     best = None
     for p in range(d.m):
         line = _pivot_line(eng, d, p, float(lam))

@@ -255,6 +255,61 @@ CSV_CASES = {
 }
 
 
+def tableau_cases():
+    """pivot_tableau (ratios.py:109-135) of every pivot and dual_certificate
+    (oracle.py:141-174) of every column's optimum -- and of two refuted values --
+    at four penalties, on the toy, ragged random instances with exact zeros,
+    -0.0 and ties, and a 300x12 grid-quantised line."""
+    from l1line.fit import solve_column
+    from l1line.oracle import OptimalityRefuted, dual_certificate
+    from l1line.ratios import EmptyPivotError, build_column, pivot_tableau
+    rng = np.random.default_rng(7)
+    mats = {"toy": np.array([[4.0, -2.0, 3.0, -6.0], [-3.0, 4.0, 2.0, -1.0], [2.0, 3.0, -3.0, -2.0],
+                             [-3.0, 4.0, 2.0, 3.0], [5.0, 3.0, 2.0, -1.0]])}
+    for t in range(6):
+        n, m = int(rng.integers(3, 40)), int(rng.integers(2, 7))
+        X = np.round(rng.uniform(-5, 5, size=(n, m)) * 2) / 2
+        X[rng.random(X.shape) < 0.2] = 0.0
+        X[rng.random(X.shape) < 0.1] = -0.0
+        if t == 5:
+            X[:, 0] = 0.0
+        mats[f"rand{t}"] = X
+    d, _ = l1line.gen_line_data(12, 300, seed=4, noise_scale=1.0)
+    mats["grid300"] = np.round(d.values * 2**10) / 2**10
+    out = {"names": np.array(sorted(mats))}
+    for name, X in mats.items():
+        dm = l1line.DataMatrix(X)
+        out[f"{name}_X"] = X
+        n, m = X.shape
+        T = float(np.abs(X).sum(axis=0).max())
+        lams = [0.0, 0.5, 0.2 * T, 2.0 * T]
+        out[f"{name}_lams"] = np.array(lams)
+        cert = []  # rows: pivot, target, lam index, case (0 optimum, 1/2 perturbed), ok, gamma, pi...
+        for p in range(m):
+            try:
+                tab = pivot_tableau(dm, p)
+            except EmptyPivotError:
+                out[f"{name}_p{p}_empty"] = np.array(1)
+                continue
+            for key in ("ratios", "weights", "source_rows", "prefix", "prefix_prev", "totals", "targets"):
+                out[f"{name}_p{p}_{key}"] = getattr(tab, key)
+            for j in range(m):
+                if j == p or (name == "grid300" and p > 1):  # certificates of two pivots there (size)
+                    continue
+                col = build_column(dm, p, j)
+                for li, lam in enumerate(lams):
+                    v = solve_column(col, lam)
+                    for case, val in enumerate((v, v + 0.25, float(col.ratios[len(col) // 2]))):
+                        try:
+                            c = dual_certificate(col, val, lam)
+                            cert.append([p, j, li, case, val, 1, c.gamma] + list(c.pi))
+                        except OptimalityRefuted:
+                            cert.append([p, j, li, case, val, 0, 0.0] + [0.0] * len(col))
+        w = max(len(r) for r in cert) if cert else 7
+        out[f"{name}_cert"] = np.array([r + [0.0] * (w - len(r)) for r in cert]) if cert else np.zeros((0, 7))
+    np.savez_compressed(os.path.join(OUT, "tableau.npz"), **out)
+
+
 def csv_cases():
     """io.read_matrix / write_matrix (io.py:46-98) on edge-case files: the
     files under csv/ and the reference's outcome for each (values as hex, or
@@ -296,7 +351,8 @@ def csv_cases():
 
 if __name__ == "__main__":
     want = set(sys.argv[1:])
-    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases, path_cases, csv_cases):
+    for f in (random_small, c1_and_grid, subspace_cases, datagen_cases, breakpoint_cases, path_cases, csv_cases,
+              tableau_cases):
         if not want or f.__name__ in want:
             f()
     for f in sorted(os.listdir(OUT)):

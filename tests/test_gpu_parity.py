@@ -775,3 +775,82 @@ def test_pivot_runs_tall_pivot(n, zeros):
             right = start + 2.0 * w
             assert R[c].tobytes() == r.tobytes(), (p, j)
             assert S[c].tobytes() == start.tobytes() and T[c].tobytes() == right.tobytes(), (p, j)
+
+
+# ------------------------------------------- the sorted-ratio API (ratios.py) --
+
+def test_tableau_and_certificates_match_reference():
+    """pivot_tableau / build_column (ratios.py:40-67, 109-135) from the device
+    sort equal the reference's arrays bit for bit (ties, exact zeros, -0.0,
+    zero pivot columns -> EmptyPivotError), solve_column / window_bounds agree,
+    and dual_certificate (oracle.py:141-174) returns the reference's
+    multipliers -- or refutes exactly where it does (tests/golden/tableau.npz)."""
+    from paper_2402_16712_b200.certify import OptimalityRefuted
+    g = load_golden("tableau.npz")
+    for name in g["names"]:
+        X = g[f"{name}_X"]
+        d = l1b.DataMatrix(X)
+        n, m = X.shape
+        lams = g[f"{name}_lams"]
+        for p in range(m):
+            if f"{name}_p{p}_empty" in g.files:
+                with pytest.raises(l1b.EmptyPivotError):
+                    l1b.pivot_tableau(d, p)
+                with pytest.raises(l1b.EmptyPivotError):
+                    l1b.build_column(d, p, (p + 1) % m)
+                continue
+            tab = l1b.pivot_tableau(d, p)
+            for key in ("ratios", "weights", "source_rows", "prefix", "prefix_prev", "totals", "targets"):
+                want = g[f"{name}_p{p}_{key}"]
+                got = getattr(tab, key)
+                assert got.shape == want.shape and got.tobytes() == want.astype(got.dtype).tobytes(), (name, p, key)
+        cert = g[f"{name}_cert"]
+        for row in cert:
+            p, j, li, case, val, ok, gamma = int(row[0]), int(row[1]), int(row[2]), int(row[3]), row[4], row[5], row[6]
+            col = l1b.build_column(d, p, j)
+            lam = float(lams[li])
+            if case == 0:
+                assert l1b.solve_column(col, lam) == val
+                for k in (0, len(col) - 1):
+                    lo, hi = l1b.window_bounds(col, k)
+                    assert hi == col.total_weight - 2.0 * (float(col.prefix_weights[k - 1]) if k else 0.0)
+                    assert lo == col.total_weight - 2.0 * float(col.prefix_weights[k])
+            if ok:
+                c = l1b.dual_certificate(col, float(val), lam)
+                assert c.gamma == gamma and c.pi.tobytes() == row[7:7 + len(col)].tobytes(), (name, p, j, li, case)
+            else:
+                with pytest.raises(OptimalityRefuted):
+                    l1b.dual_certificate(col, float(val), lam)
+
+
+def test_build_column_errors_like_reference():
+    """ratios.py:31-37: IndexError for out-of-range columns, ValueError for pivot == target."""
+    with pytest.raises(IndexError):
+        l1b.build_column(TOY, 4, 0)
+    with pytest.raises(IndexError):
+        l1b.build_column(TOY, 0, -1)
+    with pytest.raises(ValueError):
+        l1b.build_column(TOY, 2, 2)
+    with pytest.raises(IndexError):
+        l1b.pivot_tableau(TOY, 9)
+    col = l1b.build_column(TOY, 0, 3)  # pkg/tests/test_ratios.py:8-17
+    assert col.ratios.tolist() == [-1.5, -1.0, -1.0, -0.2, 1.0 / 3.0]
+    assert col.weights.tolist() == [4.0, 2.0, 3.0, 5.0, 3.0] and col.source_rows.tolist() == [0, 2, 3, 4, 1]
+    assert col.prefix_weights.tolist() == [4.0, 6.0, 9.0, 14.0, 17.0] and col.total_weight == 17.0
+    with pytest.raises(IndexError):
+        l1b.window_bounds(col, 5)
+
+
+def test_engine_cache_reuses_upload():
+    """fit_for_pivot over every pivot of one DataMatrix uploads X once (the device
+    replica is cached by the read-only values array) and matches fit_line's pivot."""
+    from paper_2402_16712_b200 import api
+    d, _ = l1b.gen_line_data(40, 300, seed=2, noise_scale=1.0)
+    api._ENGINES.clear()
+    lines = [l1b.fit_for_pivot(d, p, 1.0) for p in range(d.m)]
+    assert len(api._ENGINES) == 1
+    best = min(range(d.m), key=lambda p: (lines[p].objective, p))
+    assert l1b.fit_line(d, 1.0).preserved == best and len(api._ENGINES) == 1
+    w = np.array(d.values)  # a writable copy is never cached
+    l1b.fit_for_pivot(w, 0, 1.0)
+    assert len(api._ENGINES) == 1
