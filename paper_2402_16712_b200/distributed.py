@@ -45,10 +45,18 @@ def _comm_device(group=None) -> torch.device:
 
 
 def combine_winners(local: list[PivotWinner | None], m: int, group=None) -> list[PivotWinner]:
-    """Global winner per lambda from every rank's shard winner.
+    """Global winner per lambda from every rank's shard winner: two collectives
+    for any number of penalties.
 
-    ``local[l]`` is None when the rank owns no pivots.  Ties on the exact
-    objective go to the smallest pivot, as the sequential strict '<' does.
+    1. one ``all_gather`` of every rank's [L][5] (objective, pivot, error,
+       penalty norm, lambda) records; every rank takes the lexicographic
+       minimum of (objective, pivot) per lambda -- the strict '<' in
+       ascending pivot order of fit.py:98-102 (``local[l]`` is None when the
+       rank owns no pivot that can win);
+    2. one ``all_reduce(SUM)`` of an [L][m] int64 tensor holding, in each
+       lambda's row, the bit pattern of the winning direction on its owning
+       rank and zeros elsewhere: integer sums with one nonzero term are exact,
+       so every rank receives the owners' bytes (-0.0 included).
     """
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
@@ -63,7 +71,7 @@ def combine_winners(local: list[PivotWinner | None], m: int, group=None) -> list
     gathered = [torch.empty_like(rec) for _ in range(world)]
     dist.all_gather(gathered, rec, group=group)
     allr = torch.stack(gathered).cpu().numpy()  # [world][L][5]
-    out = []
+    owner = []
     for l in range(L):
         best_r = -1
         for r in range(world):
@@ -78,34 +86,58 @@ def combine_winners(local: list[PivotWinner | None], m: int, group=None) -> list
                 best_r = r
         if best_r < 0:
             raise ValueError("no rank owns any pivot")
-        v = torch.empty(m, dtype=torch.float64, device=dev)
-        if me == best_r:
-            v.copy_(torch.from_numpy(np.ascontiguousarray(local[l].v)).to(dev))
-        src = dist.get_global_rank(group, best_r) if group is not None else best_r
-        dist.broadcast(v, src=src, group=group)
-        z, p, e, pn, lam = allr[best_r, l]
-        out.append(PivotWinner(int(p), float(lam), v.cpu().numpy().copy(), float(e), float(pn), float(z)))
+        owner.append(best_r)
+    bits = np.zeros((L, m), dtype=np.int64)
+    for l in range(L):
+        if owner[l] == me:
+            bits[l] = np.ascontiguousarray(local[l].v, dtype=np.float64).view(np.int64)
+    vb = torch.from_numpy(bits).to(dev)
+    dist.all_reduce(vb, op=dist.ReduceOp.SUM, group=group)
+    V = vb.cpu().numpy().view(np.float64)
+    out = []
+    for l in range(L):
+        z, p, e, pn, lam = allr[owner[l], l]
+        out.append(PivotWinner(int(p), float(lam), V[l].copy(), float(e), float(pn), float(z)))
     return out
 
 
-def ub_exchange(group=None) -> Callable[[float], float]:
-    """all-reduce(MIN) of one upper bound per call (the pruning threshold)."""
+def ub_exchange(group=None) -> Callable:
+    """all-reduce(MIN) of the shards' best upper bounds: one value (a single
+    penalty) or a vector (every penalty of a sweep) per call, one collective."""
     dev = _comm_device(group)
 
-    def exchange(top: float) -> float:
-        t = torch.tensor([top], dtype=torch.float64, device=dev)
+    def exchange(top):
+        arr = np.atleast_1d(np.asarray(top, dtype=np.float64))
+        t = torch.from_numpy(arr.copy()).to(dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
-        return float(t.item())
+        out = t.cpu().numpy()
+        return float(out[0]) if np.ndim(top) == 0 else out
     return exchange
+
+
+def exchange_calls(lams, prune: bool) -> list[int]:
+    """The ub_exchange calls a pruning shard makes for ``lams``, as vector
+    lengths (engine.DeviceFit.shard_winners' paths): one scalar for a single
+    penalty, one vector over the distinct finite penalties of an all-finite
+    sweep, else one scalar per penalty.  A rank without pivots makes the same
+    calls with +inf so the collectives stay matched."""
+    lam = np.atleast_1d(np.asarray(lams, dtype=np.float64))
+    if not prune:
+        return []
+    if lam.size == 1:
+        return [0]
+    uniq = np.unique(lam[np.isfinite(lam)])
+    if uniq.size > 1 and np.all(np.isfinite(lam)):
+        return [int(uniq.size)]
+    return [0] * int(lam.size)
 
 
 def _shard_solve(eng: DeviceFit | None, lams, p_begin, p_stride, npiv, prune: bool, group=None):
     """One shard's winners; a rank without pivots still joins the exchanges."""
     ex = ub_exchange(group) if prune else None
     if npiv == 0:
-        if ex is not None:
-            for _ in lams:
-                ex(float("inf"))
+        for size in exchange_calls(lams, prune):
+            ex(float("inf") if size == 0 else np.full(size, np.inf))
         return [None] * len(lams)
     return eng.shard_winners(lams, p_begin, p_stride, npiv, prune=prune, ub_exchange=ex)
 

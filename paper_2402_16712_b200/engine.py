@@ -335,13 +335,12 @@ class DeviceFit:
         penalty's survivors are refined and fitted together as one entry list
         (one launch per cascade level instead of one per penalty)."""
         L = uniq.size
-        tops, ent_l, ent_k = np.empty(L), [], []
+        tops = np.array([float(np.min(ubm[i])) for i in range(L)])
+        if ub_exchange is not None:  # every penalty's best upper bound over all shards, one collective
+            tops = np.asarray(ub_exchange(tops), dtype=np.float64).reshape(L)
+        ent_l, ent_k = [], []
         for i in range(L):
-            top = float(np.min(ubm[i]))
-            if ub_exchange is not None:
-                top = float(ub_exchange(top))
-            tops[i] = top
-            k = np.nonzero(~(lbm[i] > self._prune_threshold(top)))[0]
+            k = np.nonzero(~(lbm[i] > self._prune_threshold(tops[i])))[0]
             ent_l.append(np.full(k.size, i, dtype=np.int64))
             ent_k.append(k)
         # entry lists are bounded by the workspace's pivot capacity: penalties
@@ -532,7 +531,8 @@ class DeviceFit:
         ``ub_exchange(top) -> global top`` (sharded fits) replaces the
         shard's best upper bound by the best over all shards before pruning;
         a shard whose pivots are all provably beaten then returns None for
-        that lambda.  Every rank must call it once per lambda when pruning.
+        that lambda.  Called once per lambda, or once with the vector of a
+        sweep's distinct penalties (distributed.exchange_calls).
         """
         lam = np.atleast_1d(np.asarray(lams, dtype=np.float64))
         if npiv is None:

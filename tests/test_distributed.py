@@ -85,11 +85,15 @@ def _exchange_worker(rank, world, port, q):
         ex = ub_exchange()
         tops = [5.0 + rank, float("inf") if rank == 1 else 2.0 - rank, 1e300 * (rank + 1)]
         got = [ex(t) for t in tops]
-        # a rank that owns no pivots still joins one exchange per lambda
+        # a rank that owns no pivots still joins the exchanges the others make:
+        # one vector for an all-finite sweep, one scalar per penalty otherwise
         if rank == world - 1:
-            none = _shard_solve(None, [0.0, 1.0], 0, 1, 0, True)
+            none = _shard_solve(None, [0.0, 1.0, 1.0], 0, 1, 0, True)
+            assert none == [None, None, None]
+            none = _shard_solve(None, [0.0, float("inf")], 0, 1, 0, True)
             assert none == [None, None]
         else:
+            got += [float(x) for x in ex(np.array([float(rank), -float(rank)]))]
             got += [ex(float(rank)), ex(-float(rank))]
         q.put((rank, got))
     finally:
@@ -113,4 +117,57 @@ def test_ub_exchange_is_global_min(world):
     for r in range(world):
         assert res[r][:3] == want
         if r != world - 1:
-            assert res[r][3:] == [0.0, -float(world - 2)]
+            assert res[r][3:] == [0.0, -float(world - 2), 0.0, -float(world - 2)]
+
+
+def test_exchange_calls_follow_the_shard_paths():
+    from paper_2402_16712_b200.distributed import exchange_calls
+    assert exchange_calls([1.0], True) == [0]
+    assert exchange_calls([0.0, 1.0, 1.0, 3.0], True) == [3]       # one vector over distinct penalties
+    assert exchange_calls([0.0, float("inf")], True) == [0, 0]     # per-penalty loop
+    assert exchange_calls([2.0, 2.0], True) == [0, 0]
+    assert exchange_calls([0.0, 1.0], False) == []
+
+
+def _combine_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2402_16712_b200.distributed import combine_winners
+        m = 5
+        v = np.array([1.0, -0.0, 0.0, -2.5, 3.0]) * (rank + 1)
+        v[0] = 1.0
+        # penalty 0: rank 1 wins outright; penalty 1: tie on the objective -> the smaller pivot
+        # (rank 0); penalty 2: rank 0 owns no candidate
+        local = [PivotWinner(rank, 0.0, v, 1.0, 2.0, 10.0 - rank),
+                 PivotWinner(10 + rank, 1.0, v, 1.0, 2.0, 7.0),
+                 None if rank == 0 else PivotWinner(20 + rank, 2.0, v, 1.0, 2.0, 3.0 + rank)]
+        out = combine_winners(local, m)
+        q.put((rank, [(w.pivot, w.v.tobytes(), w.objective) for w in out]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_combine_winners_two_collectives_keep_signed_zeros():
+    """One all_gather of the records plus one integer all_reduce of the winners'
+    bit patterns carries every winning direction byte for byte (-0.0 too)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_combine_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+
+    def vb(r):
+        v = np.array([1.0, -0.0, 0.0, -2.5, 3.0]) * (r + 1)
+        v[0] = 1.0
+        return v.tobytes()
+    want = [(world - 1, vb(world - 1), 10.0 - (world - 1)), (10, vb(0), 7.0), (21, vb(1), 4.0)]
+    for r in range(world):
+        assert res[r] == want
