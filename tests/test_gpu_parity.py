@@ -854,3 +854,28 @@ def test_engine_cache_reuses_upload():
     w = np.array(d.values)  # a writable copy is never cached
     l1b.fit_for_pivot(w, 0, 1.0)
     assert len(api._ENGINES) == 1
+
+
+def test_bounds_and_fits_deterministic_across_runs():
+    """compute-sanitizer is closed on this GPU pool (profiles/r02/compute_sanitizer_refused.txt),
+    so races are caught by determinism: k_bound's bounds are exact integer sums and
+    every exact result a fixed-order reduction, so a TMA-ring or histogram race
+    would change bytes between identical runs (tools/race_stress.py runs 40 reps)."""
+    import hashlib
+    d, _ = l1b.gen_line_data(300, 3000, seed=9, noise_scale=1.0)
+    X = np.array(d.values)
+    eng = DeviceFit(X)
+    T = float(np.abs(X).sum(axis=0).max())
+
+    def run():
+        h = hashlib.blake2b(digest_size=16)
+        lb, ub = eng.bound_pivots(1.0)
+        clb, cub = eng.bound_columns(eng.m)
+        for a in (lb, ub, clb, cub, *eng.bound_pivots_multi([0.0, 1.0, 0.3 * T])[:2]):
+            h.update(np.ascontiguousarray(a).tobytes())
+        w = eng.shard_winners([1.0])[0]
+        h.update(w.v.tobytes())
+        return h.hexdigest()
+    first = run()
+    for _ in range(4):
+        assert run() == first
