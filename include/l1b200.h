@@ -306,6 +306,19 @@ int l1b_merge_path(const double* X, int64_t n, int64_t m, const double* lambdas,
                    int64_t* o_piv, double* o_v, double* o_err, double* o_pen, double* o_obj, double* o_zlo,
                    double* o_zhi, int64_t* count);
 
+/* Algorithm 3 with its data-parallel parts on the device (csrc/merge_dev.cuh),
+ * the same arguments and bit-identical results as l1b_merge_path but X on the
+ * device (d_X, after l1b_prepare on d_ws): every event's column error, every
+ * pivot's running (sum colerr, sum |v|), every grid interval's crossing
+ * analysis and probe minima run as kernels; the host keeps the sequential
+ * segment walk; the segment lines' residuals are batched on the device.
+ * Scratch is stream-ordered (cudaMallocAsync on `stream`). */
+int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double* lambdas, int64_t K,
+                          const int64_t* piv, int64_t np_, const int64_t* deg, int64_t nd, const int64_t* ev_off,
+                          const int64_t* ev_p, const int64_t* ev_t, const double* ev_v, int64_t cap, double* o_lo,
+                          double* o_hi, int64_t* o_piv, double* o_v, double* o_err, double* o_pen, double* o_obj,
+                          double* o_zlo, double* o_zhi, int64_t* count, void* d_ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -173,26 +173,38 @@ def _snap_indices(lambdas: np.ndarray, bps: np.ndarray) -> np.ndarray:
     return np.where(here, idx, idx - 1)
 
 
-def merge_path(lambdas, solutions: PivotSolutions, data) -> SolutionPath:
-    """Lower envelope of the per-pivot objectives across the weight grid
-    (path.py:166-277), in C++ (``l1b_merge_path``)."""
-    import ctypes
-
-    from . import _lib
-    d = _as_data(data)
-    X = np.ascontiguousarray(d.values, dtype=np.float64)
-    lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64))
-    piv = np.asarray(sorted(solutions.pivots), dtype=np.int64)
-    deg = np.asarray(sorted(solutions.degenerate), dtype=np.int64)
+def _events(solutions: PivotSolutions):
+    """(pivot, target, value, breakpoint) of every entry in the reference's
+    insertion order: pivot, target, entry (path.py:193-196)."""
     ep, et, ev, eb = [], [], [], []
-    for p in piv.tolist():  # the reference's event order: pivot, target, entry
+    for p in sorted(solutions.pivots):
         for t, entries in solutions.pivots[p].entries.items():
             for bp, val in entries:
                 ep.append(p)
                 et.append(t)
                 ev.append(val)
                 eb.append(bp)
-    k = _snap_indices(lam, np.asarray(eb, dtype=np.float64)) if eb else np.zeros(0, dtype=np.int64)
+    return (np.asarray(ep, dtype=np.int64), np.asarray(et, dtype=np.int64), np.asarray(ev, dtype=np.float64),
+            np.asarray(eb, dtype=np.float64))
+
+
+def merge_path(lambdas, solutions: PivotSolutions, data) -> SolutionPath:
+    """Lower envelope of the per-pivot objectives across the weight grid
+    (path.py:166-277) on the device (``l1b_merge_path_device``)."""
+    d = _as_data(data)
+    return _merge(_engine(data, d), d, np.asarray(lambdas, dtype=np.float64),
+                  np.asarray(sorted(solutions.pivots), dtype=np.int64),
+                  np.asarray(sorted(solutions.degenerate), dtype=np.int64), *_events(solutions))
+
+
+def _merge(eng: DeviceFit, d: DataMatrix, lambdas, piv, deg, ep, et, ev, eb) -> SolutionPath:
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    lam = np.ascontiguousarray(lambdas, dtype=np.float64)
+    k = _snap_indices(lam, eb) if eb.size else np.zeros(0, dtype=np.int64)
     order = np.argsort(k, kind="stable")  # grouped by grid index, insertion order kept
     ep = np.ascontiguousarray(np.asarray(ep, dtype=np.int64)[order])
     et = np.ascontiguousarray(np.asarray(et, dtype=np.int64)[order])
@@ -207,13 +219,15 @@ def merge_path(lambdas, solutions: PivotSolutions, data) -> SolutionPath:
         opiv = np.empty(cap, dtype=np.int64)
         ov = np.empty((cap, d.m))
         cnt = ctypes.c_int64()
-        rc = lib.l1b_merge_path(
-            X.ctypes.data_as(pd), d.n, d.m, lam.ctypes.data_as(pd), lam.size, piv.ctypes.data_as(p64), piv.size,
-            deg.ctypes.data_as(p64), deg.size, off.ctypes.data_as(p64), ep.ctypes.data_as(p64),
-            et.ctypes.data_as(p64), ev.ctypes.data_as(pd), cap, o["lo"].ctypes.data_as(pd),
-            o["hi"].ctypes.data_as(pd), opiv.ctypes.data_as(p64), ov.ctypes.data_as(pd), o["err"].ctypes.data_as(pd),
-            o["pen"].ctypes.data_as(pd), o["obj"].ctypes.data_as(pd), o["zlo"].ctypes.data_as(pd),
-            o["zhi"].ctypes.data_as(pd), ctypes.byref(cnt))
+        with torch.cuda.device(eng.device):
+            rc = lib.l1b_merge_path_device(
+                eng.X.data_ptr(), d.n, d.m, lam.ctypes.data_as(pd), lam.size, piv.ctypes.data_as(p64), piv.size,
+                deg.ctypes.data_as(p64), deg.size, off.ctypes.data_as(p64), ep.ctypes.data_as(p64),
+                et.ctypes.data_as(p64), ev.ctypes.data_as(pd), cap, o["lo"].ctypes.data_as(pd),
+                o["hi"].ctypes.data_as(pd), opiv.ctypes.data_as(p64), ov.ctypes.data_as(pd),
+                o["err"].ctypes.data_as(pd), o["pen"].ctypes.data_as(pd), o["obj"].ctypes.data_as(pd),
+                o["zlo"].ctypes.data_as(pd), o["zhi"].ctypes.data_as(pd), ctypes.byref(cnt), eng.ws.data_ptr(),
+                eng.ws.numel(), eng._s)
         if rc == _lib.L1B_ENOMEM and cnt.value > cap:
             cap = int(cnt.value)
             continue
@@ -228,7 +242,50 @@ def merge_path(lambdas, solutions: PivotSolutions, data) -> SolutionPath:
     return SolutionPath(tuple(segs))
 
 
+def _pivot_events(eng: DeviceFit, pivot: int):
+    """Pivot p's breakpoint entries as arrays, without building tuples:
+    (targets, weights, values) in the order of _maps (target ascending, then
+    the entries stably sorted by weight, the death entry last among equals),
+    or None for a zero pivot column."""
+    rs, st, rt = eng.pivot_runs(pivot)
+    if rs is None:
+        return None
+    m1, k = rs.shape
+    live = rt > 0.0
+    w = np.full((m1, k + 1), np.inf)
+    w[:, :k] = np.where(live, np.where(st > 0.0, st, 0.0), np.inf)
+    w[:, k] = np.maximum(0.0, rt.max(axis=1))
+    val = np.zeros((m1, k + 1))
+    val[:, :k] = rs
+    order = np.argsort(w, axis=1, kind="stable")
+    ws = np.take_along_axis(w, order, axis=1)
+    vs = np.take_along_axis(val, order, axis=1)
+    keep = np.isfinite(ws)  # the dropped (dead) runs sort last as +inf
+    targets = np.array([j for j in range(eng.m) if j != pivot], dtype=np.int64)
+    return np.broadcast_to(targets[:, None], ws.shape)[keep], ws[keep], vs[keep]
+
+
 def solution_path(data, threads: int | None = None) -> SolutionPath:
-    """Breakpoint grid plus envelope merge in one call (path.py:280-283)."""
-    lambdas, sols = major_breakpoints(data, threads)
-    return merge_path(lambdas, sols, data)
+    """Breakpoint grid plus envelope merge in one call (path.py:280-283):
+    the runs come off the device as arrays and feed the device merge
+    directly (the same entries, grid and events as major_breakpoints +
+    merge_path)."""
+    resolve_threads(threads)
+    d = _as_data(data)
+    eng = _engine(data, d)
+    piv, deg, ep, et, ev = [], [], [], [], []
+    for p in range(d.m):
+        r = _pivot_events(eng, p)
+        if r is None:
+            deg.append(p)
+            continue
+        piv.append(p)
+        ep.append(np.full(r[0].size, p, dtype=np.int64))
+        et.append(r[0])
+        ev.append((r[1], r[2]))
+    eb = np.concatenate([w for w, _ in ev]) if ev else np.zeros(0)
+    vals = np.concatenate([v for _, v in ev]) if ev else np.zeros(0)
+    lambdas = _dedup(np.concatenate((np.zeros(1), eb)))
+    return _merge(eng, d, lambdas, np.asarray(piv, dtype=np.int64), np.asarray(deg, dtype=np.int64),
+                  np.concatenate(ep) if ep else np.zeros(0, dtype=np.int64),
+                  np.concatenate(et) if et else np.zeros(0, dtype=np.int64), vals, eb)

@@ -22,7 +22,14 @@ __global__ void __launch_bounds__(512, 1) k(long iters, int active, unsigned* ou
   unsigned a[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const int bin = MODE == 5 || MODE == 7 ? 5 : ((threadIdx.x * 7 + u * 13) & 63);
+    unsigned hsh = (threadIdx.x * 2654435761u) ^ (u * 40503u + 12345u);
+    hsh ^= hsh >> 13;
+    hsh *= 0x5bd1e995u;
+    hsh ^= hsh >> 15;
+    // MODE 15: random bins; 16: half the lanes in bins 0 / 63 (k_bound's below / above slots)
+    const int rbin = MODE == 16 ? ((hsh & 3) == 0 ? 0 : ((hsh & 3) == 1 ? 63 : (int)((hsh >> 8) % 62) + 1))
+                                : (int)((hsh >> 8) & 63);
+    const int bin = MODE == 5 || MODE == 7 ? 5 : (MODE >= 15 ? rbin : ((threadIdx.x * 7 + u * 13) & 63));
     const int slot = MODE == 3 ? ((threadIdx.x & ~31) | ((lane & 15) << 1)) : (MODE >= 6 ? lane : threadIdx.x);
     a[u] = smem_u32(h + bin * 512 + (MODE == 2 ? (slot & ~1) : slot));
   }
@@ -31,7 +38,7 @@ __global__ void __launch_bounds__(512, 1) k(long iters, int active, unsigned* ou
   for (long i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (MODE == 0 || MODE == 3 || MODE >= 5) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[u]), "r"((unsigned)i + u));
+      if (MODE == 0 || MODE == 3 || (MODE >= 5 && MODE <= 7) || MODE >= 15) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[u]), "r"((unsigned)i + u));
       if (MODE == 1 && on) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a[u]), "r"((unsigned)i + u));
       if (MODE == 2)
         asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a[u]), "l"((unsigned long long)i + u));
@@ -136,5 +143,7 @@ int main() {
   rep("shfl.idx alone", run<12>(it, 32));
   rep("shfl.idx + red.u32", run<13>(it, 32));
   rep("broadcast lds.128 + 3 red.u32", run<14>(it, 32));
+  rep("red.u32, random bins per lane", run<15>(it, 32));
+  rep("red.u32, 50% of lanes in bins 0/63", run<16>(it, 32));
   return 0;
 }
