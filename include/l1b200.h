@@ -312,12 +312,21 @@ int l1b_merge_path(const double* X, int64_t n, int64_t m, const double* lambdas,
  * pivot's running (sum colerr, sum |v|), every grid interval's crossing
  * analysis and probe minima run as kernels; the host keeps the sequential
  * segment walk; the segment lines' residuals are batched on the device.
- * Scratch is stream-ordered (cudaMallocAsync on `stream`). */
+ * Scratch is stream-ordered (cudaMallocAsync on `stream`).  The *count
+ * segments come back in one malloc'ed block *o_seg of [count][8 + m]
+ * doubles (lo, hi, pivot, err, pen, obj, z_lo, z_hi, v[m]); free it with
+ * l1b_csv_free. */
+/* path.py:157-163 for E breakpoint events at once: out_order[E] = the events
+ * grouped by their snapped grid index (ascending; insertion order within a
+ * group), out_off[K+1] = group offsets.  Host arrays.  L1B_EINTERNAL when a
+ * breakpoint is not within tol of the grid (the reference's AssertionError). */
+int l1b_snap_events(const double* lambdas, int64_t K, const double* bp, int64_t E, double tol, int64_t* out_order,
+                    int64_t* out_off);
+
 int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double* lambdas, int64_t K,
                           const int64_t* piv, int64_t np_, const int64_t* deg, int64_t nd, const int64_t* ev_off,
-                          const int64_t* ev_p, const int64_t* ev_t, const double* ev_v, int64_t cap, double* o_lo,
-                          double* o_hi, int64_t* o_piv, double* o_v, double* o_err, double* o_pen, double* o_obj,
-                          double* o_zlo, double* o_zhi, int64_t* count, void* d_ws, size_t ws_bytes, void* stream);
+                          const int64_t* ev_p, const int64_t* ev_t, const double* ev_v, double** o_seg,
+                          int64_t* count, void* d_ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -98,11 +98,15 @@ __device__ double np_pairwise_dev(F f, int64_t off, int64_t cnt) {
 
 // (1b) err[e] = sum_i |x_{i,t} - val x_{i,p}| in NumPy's pairwise order over
 // the contiguous temporary of n (core.py:93 on one column).  Xc column-major.
+// Threads take the events in (pivot, target) order (pord), so a warp's lanes
+// read the same two columns in lockstep: every load is a broadcast.
 __global__ void k_mrg_event_err(const double* __restrict__ Xc, int64_t n, int64_t E,
-                                const int64_t* __restrict__ ep, const int64_t* __restrict__ et,
-                                const double* __restrict__ ev, double* __restrict__ err) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
+                                const int64_t* __restrict__ pord, const int64_t* __restrict__ ep,
+                                const int64_t* __restrict__ et, const double* __restrict__ ev,
+                                double* __restrict__ err) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= E) return;
+  const int64_t e = pord[x];
   const double* xt = Xc + et[e] * n;
   const double* xp = Xc + ep[e] * n;
   const double val = ev[e];
@@ -212,22 +216,28 @@ __global__ void __launch_bounds__(kMrgThreads) k_mrg_intervals(
     // crossing analysis (path.py:223-240)
     for (int64_t c = tid; c < NC; c += blockDim.x) {
       const double zp = z[c], sp = sl[c];
-      double blo = -INFINITY, bhi = INFINITY;
+      // four competitors per step with their own running extrema (max / min
+      // are exact, so splitting the reduction changes nothing)
+      double blo4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, bhi4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
       bool dom = false;
-      for (int64_t q = 0; q < NC; ++q) {
-        if (q == c) continue;
-        const double zq = z[q], sq = sl[q];
-        if (fabs(__dsub_rn(sq, sp)) <= 1e-9 * fmax(fmax(1.0, sp), sq)) {
-          if (zp > zq) {
-            dom = true;
-            break;
+      for (int64_t q0 = 0; q0 < NC && !dom; q0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t q = q0 + u;
+          if (q >= NC || q == c) continue;
+          const double zq = z[q], sq = sl[q];
+          const double ds = __dsub_rn(sq, sp);
+          if (fabs(ds) <= 1e-9 * fmax(fmax(1.0, sp), sq)) {
+            dom |= zp > zq;
+          } else if (sq > sp) {
+            blo4[u] = fmax(blo4[u], __ddiv_rn(__dsub_rn(zp, zq), ds));
+          } else {
+            bhi4[u] = fmin(bhi4[u], __ddiv_rn(__dsub_rn(zq, zp), __dsub_rn(sp, sq)));
           }
-        } else if (sq > sp) {
-          blo = fmax(blo, __ddiv_rn(__dsub_rn(zp, zq), __dsub_rn(sq, sp)));
-        } else {
-          bhi = fmin(bhi, __ddiv_rn(__dsub_rn(zq, zp), __dsub_rn(sp, sq)));
         }
       }
+      const double blo = fmax(fmax(blo4[0], blo4[1]), fmax(blo4[2], blo4[3]));
+      const double bhi = fmin(fmin(bhi4[0], bhi4[1]), fmin(bhi4[2], bhi4[3]));
       if (!dom) {
         if (0.0 < blo && blo < bhi && __dadd_rn(lam_k, blo) <= lam_next) st[atomicAdd(&nst, 1)] = __dadd_rn(lam_k, blo);
         else if (blo <= 0.0 && 0.0 < bhi) st[atomicAdd(&nst, 1)] = lam_k;
@@ -340,10 +350,20 @@ extern "C" {
 
 int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double* lambdas, int64_t K,
                           const int64_t* piv, int64_t np_, const int64_t* deg, int64_t nd, const int64_t* ev_off,
-                          const int64_t* ev_p, const int64_t* ev_t, const double* ev_v, int64_t cap, double* o_lo,
-                          double* o_hi, int64_t* o_piv, double* o_v, double* o_err, double* o_pen, double* o_obj,
-                          double* o_zlo, double* o_zhi, int64_t* count, void* d_ws, size_t ws_bytes, void* stream) {
-  if (!d_X || !lambdas || K < 1 || n < 1 || m < 2 || !count || np_ + nd < 1) return L1B_EINVAL;
+                          const int64_t* ev_p, const int64_t* ev_t, const double* ev_v, double** o_seg,
+                          int64_t* count, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_X || !lambdas || K < 1 || n < 1 || m < 2 || !count || !o_seg || np_ + nd < 1) return L1B_EINVAL;
+  *o_seg = nullptr;
+  const bool timing = getenv("L1B200_MERGE_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize((cudaStream_t)stream);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "merge_path_device %-28s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   Workspace w;
   const int64_t wcap = ws_capacity(n, m, ws_bytes);
   if (wcap < 1) return L1B_ENOMEM;
@@ -373,6 +393,14 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
     }
   }
   for (int64_t q = 0; q < np_; ++q) ch_off[q + 1] += ch_off[q] + 1;  // + the initial state
+  // events in (pivot slot, target) order for the column-error kernel
+  std::vector<int64_t> pord(E);
+  {
+    std::vector<int64_t> cnt((size_t)np_ * m + 1, 0);
+    for (int64_t e = 0; e < E; ++e) ++cnt[(size_t)slot_of[ev_p[e]] * m + ev_t[e] + 1];
+    for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
+    for (int64_t e = 0; e < E; ++e) pord[cnt[(size_t)slot_of[ev_p[e]] * m + ev_t[e]]++] = e;
+  }
   const int64_t NCH = ch_off[np_];
   // candidates in pivot order (path.py:215-218)
   std::vector<int64_t> cp, cs;
@@ -389,7 +417,8 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
     }
   }
   const int64_t NC = (int64_t)cp.size();
-  DevBuf<int64_t> d_ep(s), d_et(s), d_ek(s), d_ord(s), d_peoff(s), d_choff(s), d_chk(s), d_piv(s), d_cp(s), d_cs(s),
+  mark("host prep");
+  DevBuf<int64_t> d_ep(s), d_et(s), d_ek(s), d_ord(s), d_pord(s), d_peoff(s), d_choff(s), d_chk(s), d_piv(s), d_cp(s), d_cs(s),
       d_win(s), d_ok(s), d_oi(s), d_op(s);
   DevBuf<double> d_ev(s), d_err(s), d_chE(s), d_chS(s), d_col(s), d_lam(s), d_gst(s), d_oa(s), d_V(s), d_segerr(s);
   DevBuf<unsigned long long> d_on(s);
@@ -404,6 +433,7 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
   chk(d_ev.alloc(E));
   chk(d_err.alloc(E));
   chk(d_ord.alloc(E));
+  chk(d_pord.alloc(E));
   chk(d_peoff.alloc(np_ + 1));
   chk(d_choff.alloc(np_ + 1));
   chk(d_chk.alloc(NCH));
@@ -429,6 +459,7 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
   up(d_ev.p, ev_v, 8 * E);
   up(d_ek.p, ek.data(), 8 * E);
   up(d_ord.p, ord.data(), 8 * E);
+  up(d_pord.p, pord.data(), 8 * E);
   up(d_peoff.p, pe_off.data(), 8 * (np_ + 1));
   up(d_choff.p, ch_off.data(), 8 * (np_ + 1));
   up(d_piv.p, piv, 8 * np_);
@@ -437,9 +468,11 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
   up(d_cs.p, cs.data(), 8 * NC);
   chk(cudaMemsetAsync(d_on.p, 0, 8, s));
   if (ce != cudaSuccess) return L1B_ECUDA;
+  mark("uploads");
   count_launch(4);
   k_mrg_colsums<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(d_X, n, m, d_col.p);
-  if (E) k_mrg_event_err<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(w.xc, n, E, d_ep.p, d_et.p, d_ev.p, d_err.p);
+  if (E)
+    k_mrg_event_err<<<(unsigned)((E + 127) / 128), 128, 0, s>>>(w.xc, n, E, d_pord.p, d_ep.p, d_et.p, d_ev.p, d_err.p);
   const bool use_smem = 2 * m * 8 <= 96 * 1024;
   if (!use_smem) {
     chk(d_gst.alloc((size_t)2 * m * np_));
@@ -450,6 +483,7 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
     k_mrg_pivot_walk<<<(unsigned)np_, 128, use_smem ? 2 * m * 8 : 0, s>>>(
         m, d_piv.p, d_col.p, d_peoff.p, d_ord.p, d_ek.p, d_et.p, d_ev.p, d_err.p, d_choff.p, d_chk.p, d_chE.p,
         d_chS.p, d_gst.p, use_smem ? 1 : 0);
+  mark("event errors + pivot walks");
   // degen_error = np.abs(X).sum() (path.py:190): residual_error with v = 0
   double degen_error = 0.0;
   if (nd) {
@@ -471,6 +505,7 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
       K, d_lam.p, NC, d_cp.p, d_cs.p, d_choff.p, d_chk.p, d_chE.p, d_chS.p, degen_error, d_win.p, d_ok.p, d_oi.p,
       d_oa.p, d_op.p, d_on.p, ovf_cap);
   chk(cudaGetLastError());
+  mark("intervals");
   std::vector<int64_t> win(K);
   unsigned long long novf = 0;
   chk(cudaMemcpyAsync(win.data(), d_win.p, 8 * K, cudaMemcpyDeviceToHost, s));
@@ -524,9 +559,14 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
     consider(lambdas[k], win[k]);
     for (; oc < novf && ok[oidx[oc]] == k; ++oc) consider(oa[oidx[oc]], op[oidx[oc]]);
   }
+  mark("downloads + host walk");
   const int64_t S = (int64_t)segs.size();
   *count = S;
-  if (S > cap) return L1B_ENOMEM;
+  // the segments: one malloc'ed block [S][8 + m] (lo, hi, pivot, err, pen,
+  // obj, z_lo, z_hi, v[m]), freed by the caller with l1b_csv_free
+  const int64_t rec = 8 + m;
+  double* out = (double*)malloc(sizeof(double) * (size_t)std::max<int64_t>(1, S) * rec);
+  if (!out) return L1B_ENOMEM;
   // FittedLine.build of every segment line: residuals batched on the device
   std::vector<double> Vh((size_t)S * m);
   std::vector<int64_t> sp(S);
@@ -534,30 +574,99 @@ int l1b_merge_path_device(const double* d_X, int64_t n, int64_t m, const double*
     std::memcpy(Vh.data() + (size_t)i * m, segs[i].v.data(), 8 * m);
     sp[i] = segs[i].pivot;
   }
+  std::vector<double> errs(S);
   chk(d_V.alloc((size_t)S * m));
   chk(d_segerr.alloc(S));
-  if (ce != cudaSuccess) return L1B_ENOMEM;
-  up(d_V.p, Vh.data(), 8 * (size_t)S * m);
-  if (ce != cudaSuccess) return L1B_ECUDA;
-  int st = l1b_residual_exact_batch(d_X, n, m, d_V.p, m, sp.data(), S, d_segerr.p, d_ws, ws_bytes, stream);
-  if (st != L1B_OK) return st;
-  chk(cudaMemcpyAsync(o_err, d_segerr.p, 8 * S, cudaMemcpyDeviceToHost, s));
-  chk(cudaStreamSynchronize(s));
-  if (ce != cudaSuccess) return L1B_ECUDA;
+  if (ce == cudaSuccess) up(d_V.p, Vh.data(), 8 * (size_t)S * m);
+  int st = ce == cudaSuccess ? l1b_residual_exact_batch(d_X, n, m, d_V.p, m, sp.data(), S, d_segerr.p, d_ws, ws_bytes,
+                                                          stream)
+                             : L1B_ECUDA;
+  if (st == L1B_OK) {
+    chk(cudaMemcpyAsync(errs.data(), d_segerr.p, 8 * S, cudaMemcpyDeviceToHost, s));
+    chk(cudaStreamSynchronize(s));
+    if (ce != cudaSuccess) st = L1B_ECUDA;
+  }
+  if (st != L1B_OK) {
+    free(out);
+    return st;
+  }
+  mark("segment residuals");
   for (int64_t i = 0; i < S; ++i) {
     const Seg& g = segs[i];
-    const double err = o_err[i];
+    const double err = errs[i];
     const double pen = np_pairwise_f([&](int64_t j) { return fabs(g.v[j]); }, 0, m);
     const double obj = err + g.lo * pen;
-    o_lo[i] = g.lo;
-    o_hi[i] = g.hi;
-    o_piv[i] = g.pivot;
-    o_pen[i] = pen;
-    o_obj[i] = obj;
-    o_zlo[i] = obj;
-    o_zhi[i] = std::isinf(g.hi) ? (pen > 0.0 ? INFINITY : err) : err + g.hi * pen;
-    std::memcpy(o_v + (size_t)i * m, g.v.data(), 8 * m);
+    double* r = out + (size_t)i * rec;
+    r[0] = g.lo;
+    r[1] = g.hi;
+    r[2] = (double)g.pivot;
+    r[3] = err;
+    r[4] = pen;
+    r[5] = obj;
+    r[6] = obj;
+    r[7] = std::isinf(g.hi) ? (pen > 0.0 ? INFINITY : err) : err + g.hi * pen;
+    std::memcpy(r + 8, g.v.data(), 8 * m);
   }
+  *o_seg = out;
+  mark("outputs");
+  return L1B_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// path.py:157-163 for every event at once, grouped for the merge: event e's
+// breakpoint bp[e] snaps to the grid index k of lambdas[K] (ascending) with
+// |lambdas[k] - bp| <= tol (the left searchsorted position, else the one
+// before); out_order lists the events grouped by k, insertion order kept
+// within a group, and out_off[K+1] the groups' offsets.  Host code: an LSD
+// radix sort of the breakpoints, one merge sweep against the grid, a stable
+// counting sort by k (numpy's searchsorted on unsorted queries + argsort
+// took 15 s for 22 M events).  L1B_EINTERNAL if a breakpoint is off the grid.
+int l1b_snap_events(const double* lambdas, int64_t K, const double* bp, int64_t E, double tol, int64_t* out_order,
+                    int64_t* out_off) {
+  if (!lambdas || K < 1 || (E > 0 && (!bp || !out_order)) || !out_off) return L1B_EINVAL;
+  std::vector<uint64_t> key(E);
+  std::vector<int64_t> idx(E), tmp_i(E);
+  std::vector<uint64_t> tmp_k(E);
+  for (int64_t e = 0; e < E; ++e) {
+    uint64_t b;
+    const double x = bp[e] == 0.0 ? 0.0 : bp[e];  // -0.0 sorts with +0.0
+    std::memcpy(&b, &x, 8);
+    key[e] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving image of the double
+    idx[e] = e;
+  }
+  for (int pass = 0; pass < 4; ++pass) {  // 16-bit digits, stable
+    const int sh = 16 * pass;
+    std::vector<int64_t> cnt(65537, 0);
+    for (int64_t e = 0; e < E; ++e) ++cnt[((key[e] >> sh) & 0xffff) + 1];
+    for (int b = 0; b < 65536; ++b) cnt[b + 1] += cnt[b];
+    for (int64_t e = 0; e < E; ++e) {
+      const int64_t at = cnt[(key[e] >> sh) & 0xffff]++;
+      tmp_k[at] = key[e];
+      tmp_i[at] = idx[e];
+    }
+    key.swap(tmp_k);
+    idx.swap(tmp_i);
+  }
+  std::vector<int64_t> kk(E);
+  int64_t i = 0;
+  for (int64_t r = 0; r < E; ++r) {
+    const int64_t e = idx[r];
+    const double b = bp[e];
+    while (i < K && lambdas[i] < b) ++i;  // np.searchsorted(..., side="left")
+    int64_t k;
+    if (i < K && fabs(lambdas[i] - b) <= tol) k = i;
+    else if (i > 0 && fabs(lambdas[i - 1] - b) <= tol) k = i - 1;
+    else return L1B_EINTERNAL;
+    kk[e] = k;
+  }
+  std::fill(out_off, out_off + K + 1, 0);
+  for (int64_t e = 0; e < E; ++e) ++out_off[kk[e] + 1];
+  for (int64_t k = 0; k < K; ++k) out_off[k + 1] += out_off[k];
+  std::vector<int64_t> at(out_off, out_off + K);
+  for (int64_t e = 0; e < E; ++e) out_order[at[kk[e]]++] = e;
   return L1B_OK;
 }
 

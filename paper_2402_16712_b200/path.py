@@ -204,41 +204,41 @@ def _merge(eng: DeviceFit, d: DataMatrix, lambdas, piv, deg, ep, et, ev, eb) -> 
 
     from . import _lib
     lam = np.ascontiguousarray(lambdas, dtype=np.float64)
-    k = _snap_indices(lam, eb) if eb.size else np.zeros(0, dtype=np.int64)
-    order = np.argsort(k, kind="stable")  # grouped by grid index, insertion order kept
+    lib = _lib.load()
+    # events grouped by snapped grid index, insertion order kept (path.py:157-163, 193-196)
+    eb = np.ascontiguousarray(eb, dtype=np.float64)
+    order = np.empty(eb.size, dtype=np.int64)
+    off = np.empty(lam.size + 1, dtype=np.int64)
+    rc = lib.l1b_snap_events(lam.ctypes.data, lam.size, eb.ctypes.data, eb.size, DEDUP_TOL, order.ctypes.data,
+                             off.ctypes.data)
+    if rc == _lib.L1B_EINTERNAL:
+        raise AssertionError("a breakpoint is missing from the weight grid")
+    _lib.check(rc, "l1b_snap_events")
     ep = np.ascontiguousarray(np.asarray(ep, dtype=np.int64)[order])
     et = np.ascontiguousarray(np.asarray(et, dtype=np.int64)[order])
     ev = np.ascontiguousarray(np.asarray(ev, dtype=np.float64)[order])
-    off = np.ascontiguousarray(np.searchsorted(k[order], np.arange(lam.size + 1)).astype(np.int64))
-    lib = _lib.load()
     p64 = ctypes.POINTER(ctypes.c_int64)
     pd = ctypes.POINTER(ctypes.c_double)
-    cap = 64
-    while True:
-        o = {nm: np.empty(cap) for nm in ("lo", "hi", "err", "pen", "obj", "zlo", "zhi")}
-        opiv = np.empty(cap, dtype=np.int64)
-        ov = np.empty((cap, d.m))
-        cnt = ctypes.c_int64()
-        with torch.cuda.device(eng.device):
-            rc = lib.l1b_merge_path_device(
-                eng.X.data_ptr(), d.n, d.m, lam.ctypes.data_as(pd), lam.size, piv.ctypes.data_as(p64), piv.size,
-                deg.ctypes.data_as(p64), deg.size, off.ctypes.data_as(p64), ep.ctypes.data_as(p64),
-                et.ctypes.data_as(p64), ev.ctypes.data_as(pd), cap, o["lo"].ctypes.data_as(pd),
-                o["hi"].ctypes.data_as(pd), opiv.ctypes.data_as(p64), ov.ctypes.data_as(pd),
-                o["err"].ctypes.data_as(pd), o["pen"].ctypes.data_as(pd), o["obj"].ctypes.data_as(pd),
-                o["zlo"].ctypes.data_as(pd), o["zhi"].ctypes.data_as(pd), ctypes.byref(cnt), eng.ws.data_ptr(),
-                eng.ws.numel(), eng._s)
-        if rc == _lib.L1B_ENOMEM and cnt.value > cap:
-            cap = int(cnt.value)
-            continue
-        _lib.check(rc, "l1b_merge_path")
-        break
+    buf = ctypes.c_void_p()
+    cnt = ctypes.c_int64()
+    with torch.cuda.device(eng.device):
+        rc = lib.l1b_merge_path_device(
+            eng.X.data_ptr(), d.n, d.m, lam.ctypes.data_as(pd), lam.size, piv.ctypes.data_as(p64), piv.size,
+            deg.ctypes.data_as(p64), deg.size, off.ctypes.data_as(p64), ep.ctypes.data_as(p64),
+            et.ctypes.data_as(p64), ev.ctypes.data_as(pd), ctypes.byref(buf), ctypes.byref(cnt), eng.ws.data_ptr(),
+            eng.ws.numel(), eng._s)
+    _lib.check(rc, "l1b_merge_path_device")
+    S, rec = int(cnt.value), 8 + d.m
+    try:
+        raw = np.ctypeslib.as_array(ctypes.cast(buf, pd), shape=(max(1, S) * rec,))[:S * rec].reshape(S, rec).copy()
+    finally:
+        lib.l1b_csv_free(buf)
     segs = []
-    for s_ in range(int(cnt.value)):
-        line = FittedLine(v=ov[s_].copy(), preserved=int(opiv[s_]), lam=float(o["lo"][s_]), error=float(o["err"][s_]),
-                          penalty_norm=float(o["pen"][s_]), objective=float(o["obj"][s_]))
-        segs.append(PathSegment(lambda_lo=float(o["lo"][s_]), lambda_hi=float(o["hi"][s_]), line=line,
-                                z_lo=float(o["zlo"][s_]), z_hi=float(o["zhi"][s_])))
+    for r in raw:
+        line = FittedLine(v=r[8:].copy(), preserved=int(r[2]), lam=float(r[0]), error=float(r[3]),
+                          penalty_norm=float(r[4]), objective=float(r[5]))
+        segs.append(PathSegment(lambda_lo=float(r[0]), lambda_hi=float(r[1]), line=line, z_lo=float(r[6]),
+                                z_hi=float(r[7])))
     return SolutionPath(tuple(segs))
 
 
