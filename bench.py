@@ -145,34 +145,43 @@ def cpu_reference(X, lams, budget_s: float, threads: int | None = None):
     pivot per worker thread, until `budget_s` elapses or every pivot is done;
     returns (solves/s, seconds per full fit (extrapolated), sample).
     """
+    from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait
     n, m = X.shape
     threads = threads or os.cpu_count() or 1
     order = np.argsort((np.arange(m) * 0.6180339887498949) % 1.0, kind="stable")  # low-discrepancy order
     ref = _reference_package() if len(lams) == 1 else None
-    if ref is not None:  # the reference package itself: fit_for_pivot through its own thread pool
-        l1line, map_indices = ref
+    if ref is not None:  # the reference package itself: fit_for_pivot, one task per pivot
+        l1line, _ = ref
         data = l1line.DataMatrix(X)
 
-        def run(batch):
-            map_indices(lambda i: l1line.fit_for_pivot(data, int(batch[i]), float(lams[0])), batch.size, threads)
+        def one(p):
+            l1line.fit_for_pivot(data, int(p), float(lams[0]))
     else:
         import oracle
 
-        def run(batch):
-            _fit_pivot_set(oracle, X, lams, batch, threads)
-    done, t0 = 0, time.perf_counter()
-    while done < m:
-        batch = order[done:done + threads]
-        run(batch)
-        done += batch.size
-        if time.perf_counter() - t0 >= budget_s:
-            break
+        def one(p):
+            oracle.fit_pivots(X, lams, int(p), int(p) + 1, threads=1, want_v=False)
+    # a window of 2 x threads tasks in flight, refilled as they finish, until the
+    # budget is spent: every worker stays busy (no per-batch tail)
+    done, nxt, t0 = 0, 0, time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        live = set()
+        while nxt < m and len(live) < 2 * threads:
+            live.add(pool.submit(one, order[nxt]))
+            nxt += 1
+        while live:
+            fin, live = wait(live, return_when=FIRST_COMPLETED)
+            done += len(fin)
+            if time.perf_counter() - t0 < budget_s:
+                while nxt < m and len(live) < 2 * threads:
+                    live.add(pool.submit(one, order[nxt]))
+                    nxt += 1
     dt = time.perf_counter() - t0
     solves = done * (m - 1) * len(lams)
     per_fit = dt * m / done / len(lams)
     what = "l1line.fit_for_pivot (baseline/_ref)" if ref is not None else "oracle C port"
     return (solves / dt, per_fit, f"{what}: {done}/{m} pivots (evenly spread) x {len(lams)} lambda of the same "
-            f"input, {dt:.1f}s", "reference" if ref is not None else "port")
+            f"input on {threads} threads, {dt:.1f}s", "reference" if ref is not None else "port")
 
 
 def _cpu_model() -> str:
@@ -308,13 +317,16 @@ def _reference_package():
 
 
 def _run_reference_package(args, ref, X, lams, threads, world):
-    """The reference's own fit_line (fit.py:88-102) decomposed over the timed
-    steps: step k runs fit_for_pivot (fit.py:75-85) on pivots
-    [k m / K, (k + 1) m / K) through the reference's own thread pool
-    (parallel.map_indices, threads = os.cpu_count()), so one complete fit is
-    timed, every pivot exactly once; the strict-'<' argmin in pivot order
-    (fit.py:98-102) over all of them is the fit's answer.  C1 (milliseconds
-    per fit) runs l1line.fit_line itself once per step."""
+    """The reference's own fit_line (fit.py:88-102) on all host cores, timed in
+    K steps without splitting it: fit_for_pivot (fit.py:75-85) for every pivot
+    through one ThreadPoolExecutor.map over range(m) -- exactly what
+    parallel.map_indices (parallel.py:36-43) does inside fit_line -- and the
+    in-order results timestamped at the K chunk boundaries (pivot k m / K), so
+    step k is the time the fit spent between two boundaries, the steps add up
+    to one complete fit (no per-step pool start or tail), and the strict '<'
+    argmin in pivot order (fit.py:98-102) over all of them is its answer.
+    C1 (milliseconds per fit) runs l1line.fit_line itself once per step."""
+    from concurrent.futures import ThreadPoolExecutor
     l1line, map_indices = ref
     n, m = X.shape
     data = l1line.DataMatrix(X)
@@ -324,26 +336,34 @@ def _run_reference_package(args, ref, X, lams, threads, world):
     for w in range(args.warmup):  # untimed: one batch of `threads` pivots
         lo = (w * threads) % m
         map_indices(lambda i: l1line.fit_for_pivot(data, lo + i, lam), min(threads, m - lo), threads)
-    t_steps, objs, best = [], [], None
-    for k in range(K):
-        t0 = time.perf_counter()
-        if whole:
+    t_steps, best = [], None
+    if whole:
+        for k in range(K):
+            t0 = time.perf_counter()
             best = l1line.fit_line(data, lam, threads=threads)
-        else:
-            lo, hi = k * m // K, (k + 1) * m // K
-            lines = map_indices(lambda i: l1line.fit_for_pivot(data, lo + i, lam), hi - lo, threads)
-            objs.extend(lines)
-        t_steps.append(time.perf_counter() - t0)
-    if not whole:
-        best = objs[0]
-        for line in objs[1:]:
+            t_steps.append(time.perf_counter() - t0)
+    else:
+        bounds = [(k + 1) * m // K for k in range(K)]
+        lines = []
+        with ThreadPoolExecutor(max_workers=min(threads, m)) as pool:
+            t_prev = time.perf_counter()
+            nxt = 0
+            for i, line in enumerate(pool.map(lambda p: l1line.fit_for_pivot(data, p, lam), range(m))):
+                lines.append(line)
+                while nxt < K and i + 1 == bounds[nxt]:
+                    t = time.perf_counter()
+                    t_steps.append(t - t_prev)
+                    t_prev = t
+                    nxt += 1
+        best = lines[0]
+        for line in lines[1:]:
             if line.objective < best.objective:  # fit.py:98-102
                 best = line
     t_fit = float(np.mean(t_steps)) if whole else float(np.sum(t_steps))
     v = m * (m - 1) / t_fit
-    sample = (f"l1line.fit_line, a complete fit per step" if whole else
-              f"one complete l1line fit: fit_for_pivot on all {m} pivots through parallel.map_indices, "
-              f"each pivot timed once across the {K} steps")
+    sample = ("l1line.fit_line, a complete fit per step" if whole else
+              f"one complete l1line fit: fit_for_pivot on all {m} pivots through one ThreadPoolExecutor.map "
+              f"(parallel.map_indices' mechanism), timed in {K} steps at pivot boundaries k*m/K")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(t_steps)),
@@ -535,8 +555,12 @@ def run_ours(args):
 
     # ---- end to end through the public API (host numpy in, FittedLine out) --
     data = l1b.DataMatrix(X)  # built once, as the reference CLI does before timing fit_line
+    from paper_2402_16712_b200 import api as _api
     if world == 1:
         def e2e_step():
+            # no device replica carried over from the last step: every step
+            # uploads X (the library keeps one per read-only input otherwise)
+            _api.clear_device_cache()
             if ncomp > 1:
                 return l1b.fit_subspace(data, lams[0], ncomp)
             return l1b.fit_lines(data, lams)

@@ -30,7 +30,7 @@ from .core import DataMatrix, FittedLine, SubspaceFit
 from .engine import DeviceFit
 
 __all__ = ["fit_line", "fit_lines", "fit_for_pivot", "degenerate_line", "fit_subspace", "deflate",
-           "residual_error", "resolve_threads", "discordance", "l0_fraction"]
+           "residual_error", "resolve_threads", "discordance", "l0_fraction", "clear_device_cache"]
 
 THREADS_ENV = "L1LINE_THREADS"
 
@@ -94,6 +94,11 @@ def _engine(data, d: DataMatrix) -> DeviceFit:
     _ENGINES.insert(0, (weakref.ref(src), dev, eng))
     del _ENGINES[_ENGINE_SLOTS:]
     return eng
+
+
+def clear_device_cache() -> None:
+    """Drop the cached device replicas (the next call on any input uploads it again)."""
+    _ENGINES.clear()
 
 
 def _line(w) -> FittedLine:

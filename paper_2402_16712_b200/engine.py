@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -554,7 +555,7 @@ class DeviceFit:
         if uniq.size > 1 and all(np.isfinite(lam)):
             # the per-penalty next ranges (8 B per (penalty, pivot, target)) let the
             # first refinement level continue instead of re-sampling
-            keep_ranges = uniq.size * npiv * self.m * 8 <= (4 << 30)
+            keep_ranges = uniq.size * npiv * self.m * 8 <= (4 << 30) and os.environ.get("L1B200_SWEEP_RANGES", "1") != "0"
             res = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv, ranges=keep_ranges)
             lbm, ubm = res[0], res[1]
             rg = res[2] if keep_ranges else None
