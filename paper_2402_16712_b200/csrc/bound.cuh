@@ -64,6 +64,7 @@ static_assert(kBTgt == 64 || kBTgt == 128, "k_tile_q lays out 64- or 128-target 
 static_assert(kBRowsW % 2 == 0 && kBRows % kBRG == 0, "a warp takes whole row pairs of a chunk");
 static_assert(KB_FLUSH * kBRowsW <= 32, "residual summation margin (column_bounds) covers 16 row pairs");
 static_assert(kBStages * kBStage >= kBRG * kBProb * 8, "stage buffers hold the warps' residual shares");
+constexpr int kBLamGroup = 4;              // penalties per pivot-sum round of a multi-penalty epilogue
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
 // bracket half-width in sample ranks: narrow for the one-pass bound (tight
 // bins), wider when later passes refine it (fewer optima outside)
@@ -103,163 +104,191 @@ struct Prefix {
   }
 };
 
+// Bounds of one column optimum, split into the penalty-free setup (margins,
+// edge signs, the prefix sums around the sample centre) and the per-penalty
+// part, so a multi-penalty pass sets a column up once (ColumnBounds::at).
+struct ColumnBounds {
+  const Prefix& H;
+  double q, lo, hi, c, ec, T, colsum;
+  double w, dC, pert, eps, iq2, q2, dc, f0e, f0;
+  int z0, z1, kc;
+  long long CuC, SCC, CuC1, Cu0, Cu62, SC62;
+
+  __device__ __forceinline__ double edge(int k) const { return lo + (double)k * w; }
+
+  __device__ __forceinline__ ColumnBounds(const Prefix& H_, double q_, double lo_, double hi_, double c_, double ec_,
+                                          double T_, double colsum_, int64_t n)
+      : H(H_), q(q_), lo(lo_), hi(hi_), c(c_), ec(ec_), T(T_), colsum(colsum_) {
+    w = (hi - lo) / (double)kNI;
+    // margins: the 32-bit weights are within q/2 of |x_ip| each (so any
+    // cumulative weight within n q / 2), the residual terms within 2^-22 of
+    // |a| + |c b|, and their per-chunk float sums
+    dC = 0.5000001 * (double)n * q;
+    // every row's float ratio (and the float bin edges) sit within pert / w_i
+    // of its binned position, so f moves by at most pert when the rows are
+    // moved into their bins; the bounds below hold for that moved problem
+    pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
+    // (k_bound: each thread's FP32 accumulator takes <= 16 two-row sums between
+    // FP64 flushes, KB_FLUSH: relative error <= 17 u)
+    eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
+    // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
+    // (slots 0..k).  The subgradient bounds at edge k are
+    //   glo(k) = 2 (C_k - dC) - T + lam sp(k) <= g(e_k+),  sp(k) = e_k >= 0 ? 1 : -1,
+    //   ghi(k) = 2 (C_k + dC) - T + lam sm(k) >= g(e_k-),  sm(k) = e_k >  0 ? 1 : -1,
+    // on bin [e_k, e_k+1] g lies in [glo(k), ghi(k+1)], and their integrals
+    //   Ilo(k) = sum_{q<k} w glo(q),  Ihi(k) = sum_{q<k} w ghi(q+1)
+    // need only the exact integer prefix sums Cu_k, SC_k = sum_{q<k} Cu_q and
+    // the edge-sign counts, so the walk over the edges is integer-only.
+    z0 = min(kNB - 1, max(0, (int)ceil(-lo / w)));  // edges e_0 .. e_z0-1 are < 0
+    while (z0 > 0 && edge(z0 - 1) >= 0.0) --z0;
+    while (z0 < kNB - 1 && edge(z0) < 0.0) ++z0;
+    z1 = z0;  // edges e_0 .. e_z1-1 are <= 0
+    while (z1 < kNB - 1 && edge(z1) <= 0.0) ++z1;
+    kc = min(kNI - 1, max(0, (int)floor((c - lo) / w)));
+    iq2 = 0.5 / q;
+    q2 = 2.0 * q;
+    CuC = H.cu(kc);
+    SCC = (long long)H.sc(kc);
+    CuC1 = H.cu(kc + 1);
+    Cu0 = H.cu(0);
+    Cu62 = H.cu(kNI);
+    SC62 = (long long)H.sc(kNI);
+    dc = c - edge(kc);
+    // f(0) = sum_i |x_ij|: the dead value; colsum carries the rounding of an
+    // n-term f64 sum (any order): within (n + 128) 2^-53 of it
+    f0e = (double)(n + 128) * 0x1p-53 * colsum;
+    f0 = colsum - f0e;  // a lower bound of f(0) (the kink bounds below)
+  }
+
+  __device__ __forceinline__ void at(double lam, float smin, float smax, double* lbo, double* ubo, double2* range,
+                                     float2* next) const {
+    const double fc = ec + lam * fabs(c);
+    // integer thresholds, rounded so that passing them implies the double test:
+    // ghi(k) <= 0 <=> Cu_k <= (T - 2 dC - lam sm) / 2q;  glo(k) >= 0 <=> Cu_k >= (T + 2 dC - lam sp) / 2q
+    auto thr_le = [&](double x) -> long long {
+      x = x * iq2 * (1.0 - 0x1p-44) - 0x1p-8;
+      return x < 0.0 ? -1LL : (x >= 0x1p62 ? (1LL << 62) : (long long)floor(x));
+    };
+    auto thr_ge = [&](double x) -> long long {
+      x = x * iq2 * (1.0 + 0x1p-44) + 0x1p-8;
+      return x <= 0.0 ? 0LL : (x >= 0x1p62 ? (1LL << 62) : (long long)ceil(x));
+    };
+    const long long tLm = thr_le(T - 2.0 * dC + lam), tLp = thr_le(T - 2.0 * dC - lam);  // sm = -1 / +1
+    const long long tRm = thr_ge(T + 2.0 * dC + lam), tRp = thr_ge(T + 2.0 * dC - lam);  // sp = -1 / +1
+    // kL = last edge with ghi <= 0, kR = first with glo >= 0: Cu_k grows and
+    // the thresholds only drop at the sign change, so both tests are monotone
+    // in k and two binary searches over the prefix sums find them
+    const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
+    const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
+    const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
+    const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
+    auto pL = [&](int k) {
+      const unsigned cu = H.cu(k);
+      return k >= z1 ? (hasL_p & (cu <= uLp)) : (hasL_m & (cu <= uLm));
+    };
+    auto pR = [&](int k) {
+      const unsigned cu = H.cu(k);
+      return k >= z0 ? (hasR_p & (cu >= uRp)) : (hasR_m & (cu >= uRm));
+    };
+    int kL, kR;
+    {
+      int a = -1, b = kNI + 1;  // pL(a) holds, pL(b) fails
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (pL(mid)) a = mid;
+        else b = mid;
+      }
+      kL = a;
+      a = -1;
+      b = kNI + 1;  // pR(a) fails, pR(b) holds
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (pR(mid)) b = mid;
+        else a = mid;
+      }
+      kR = b;  // kNI + 1 = kNB - 1: not in the bracket
+    }
+    const long long CuL = kL >= 0 ? (long long)H.cu(kL) : 0, SCL = kL >= 0 ? (long long)H.sc(kL) : 0;
+    const long long CuR = kR <= kNI ? (long long)H.cu(kR) : 0, SCR = kR <= kNI ? (long long)H.sc(kR) : 0;
+    auto glo = [&](int k, long long Cu) { return q2 * (double)Cu - 2.0 * dC - T + (k >= z0 ? lam : -lam); };
+    auto ghi = [&](int k, long long Cu) { return q2 * (double)Cu + 2.0 * dC - T + (k >= z1 ? lam : -lam); };
+    auto Ilo = [&](int k, long long SC) {  // SP(k) = sum_{q<k} sp(q) = k - 2 min(k, z0)
+      return w * (q2 * (double)SC - (double)k * (2.0 * dC + T) + lam * (double)(k - 2 * min(k, z0)));
+    };
+    auto Ihi = [&](int k, long long SC, long long Cu) {  // SM1(k) = sum_{q=1..k} sm(q)
+      const int le = max(0, min(k, z1 - 1));
+      return w * (q2 * (double)(SC + Cu - Cu0) + (double)k * (2.0 * dC - T) + lam * (double)(k - 2 * le));
+    };
+    const double IloC = Ilo(kc, SCC), IhiC = Ihi(kc, SCC, CuC);
+    const double gloC = glo(kc, CuC), ghiC = ghi(kc + 1, CuC1), gloL = kL >= 0 ? glo(kL, CuL) : 0.0;
+    const double CL = q * (double)CuL, CR = kR <= kNI ? q * (double)CuR : T;
+    // f at e_kc from f(c), then at any edge k from e_kc
+    const double fkc_lo = fc - dc * ghiC, fkc_hi = fc - dc * gloC;
+    auto f_lo = [&](int k, long long SC, long long Cu) {
+      return k >= kc ? fkc_lo + (Ilo(k, SC) - IloC) : fkc_lo - (IhiC - Ihi(k, SC, Cu));
+    };
+    auto f_hi = [&](int k, long long SC, long long Cu) {
+      return k >= kc ? fkc_hi + (Ihi(k, SC, Cu) - IhiC) : fkc_hi - (IloC - Ilo(k, SC));
+    };
+    double lb, ub = fmin(fc + eps, colsum + f0e);
+    const double eL = kL >= 0 ? edge(kL) : -INFINITY, eR = kR <= kNI ? edge(kR) : INFINITY;
+    if (kL >= 0 && kR <= kNI && kL <= kR) {
+      lb = f_lo(kL, SCL, CuL) - eps + fmin(0.0, gloL) * (eR - eL);
+      ub = fmin(ub, fmin(f_hi(kL, SCL, CuL), f_hi(kR, SCR, CuR)) + eps);
+    } else {
+      lb = 0.0;  // the optimum lies beyond the bracket: only the trivial bound
+      if (kL == kNI) ub = fmin(ub, f_hi(kNI, SC62, Cu62) + eps);
+    }
+    if (eL <= 0.0 && 0.0 <= eR) {
+      // the penalty's kink: g(0-) <= 2 W(r < eR) - T - lam, g(0+) >= 2 W(r < eL) - T + lam;
+      // f(v) >= f0 + g(0-) v on v <= 0 and f(v) >= f0 + g(0+) v on v >= 0
+      const double g0m = 2.0 * (CR + dC) - T - lam, g0p = 2.0 * ((kL >= 0 ? CL : 0.0) - dC) - T + lam;
+      const double left = isfinite(eL) ? f0 + fmax(0.0, g0m) * eL : (g0m <= 0.0 ? f0 : 0.0);
+      const double right = isfinite(eR) ? f0 + fmin(0.0, g0p) * eR : (g0p >= 0.0 ? f0 : 0.0);
+      lb = fmax(lb, fmin(left, right) - pert);
+    }
+    *lbo = fmax(0.0, lb);
+    *ubo = ub;
+    // where the optimum lies (seed for the exact solver), widened for the
+    // rows' float ratios and edges
+    if (range) {
+      if (kL >= 0 && kR <= kNI && kL <= kR) {
+        const double d = 0x1p-19 * (fabs(eL) + fabs(eR) + fabs(lo) + fabs(hi)) + 0x1p-10 * w;
+        *range = make_double2(eL - d, eR + d);
+      } else {
+        *range = make_double2(-INFINITY, INFINITY);
+      }
+    }
+    // the next pass's range: between the edges where the optimum provably lies
+    // (a little wider), or, when a side is not in the bracket, extended there
+    const float flo = (float)lo, fhi = (float)hi, span = fhi - flo;
+    float a, b;
+    if (kL >= 0 && kR <= kNI) {
+      a = (float)edge(max(0, min(kL, kR - 1)));
+      b = (float)edge(min(kNI, max(kR, kL + 1)));
+    } else if (kR <= kNI) {  // optimum at or below lo
+      a = fminf(smin, flo) - 2.f * span;
+      b = (float)edge(kR);
+    } else if (kL >= 0) {  // at or above the last edge
+      a = (float)edge(kL);
+      b = fmaxf(smax, fhi) + 2.f * span;
+    } else {  // no edge is decisive (margins dominate): keep the range
+      a = flo;
+      b = fhi;
+    }
+    const float mg = 0.05f * (b - a);
+    a -= mg;
+    b += mg;
+    if (!(b > a)) b = a + fmaxf(fabsf(a), 1e-30f) * 1e-6f;
+    *next = make_float2(a, b);
+  }
+};
+
 __device__ __forceinline__ void column_bounds(const Prefix& H, double q, double lo, double hi, double c,
                                               double ec, double T, double lam, double colsum, int64_t n,
                                               float smin, float smax, double* lbo, double* ubo, double2* range,
                                               float2* next) {
-  const double w = (hi - lo) / (double)kNI;
-  // margins: the 32-bit weights are within q/2 of |x_ip| each (so any
-  // cumulative weight within n q / 2), the residual terms within 2^-22 of
-  // |a| + |c b|, and their per-chunk float sums
-  const double dC = 0.5000001 * (double)n * q;
-  // every row's float ratio (and the float bin edges) sit within pert / w_i
-  // of its binned position, so f moves by at most pert when the rows are
-  // moved into their bins; the bounds below hold for that moved problem
-  const double pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
-  // (k_bound: each thread's FP32 accumulator takes <= 16 two-row sums between
-  // FP64 flushes, KB_FLUSH: relative error <= 17 u)
-  const double eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
-  const double fc = ec + lam * fabs(c);
-  // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
-  // (slots 0..k).  The subgradient bounds at edge k are
-  //   glo(k) = 2 (C_k - dC) - T + lam sp(k) <= g(e_k+),  sp(k) = e_k >= 0 ? 1 : -1,
-  //   ghi(k) = 2 (C_k + dC) - T + lam sm(k) >= g(e_k-),  sm(k) = e_k >  0 ? 1 : -1,
-  // on bin [e_k, e_k+1] g lies in [glo(k), ghi(k+1)], and their integrals
-  //   Ilo(k) = sum_{q<k} w glo(q),  Ihi(k) = sum_{q<k} w ghi(q+1)
-  // need only the exact integer prefix sums Cu_k, SC_k = sum_{q<k} Cu_q and
-  // the edge-sign counts, so the walk over the edges is integer-only.
-  auto edge = [&](int k) { return lo + (double)k * w; };
-  int z0 = min(kNB - 1, max(0, (int)ceil(-lo / w)));  // edges e_0 .. e_z0-1 are < 0
-  while (z0 > 0 && edge(z0 - 1) >= 0.0) --z0;
-  while (z0 < kNB - 1 && edge(z0) < 0.0) ++z0;
-  int z1 = z0;  // edges e_0 .. e_z1-1 are <= 0
-  while (z1 < kNB - 1 && edge(z1) <= 0.0) ++z1;
-  const int kc = min(kNI - 1, max(0, (int)floor((c - lo) / w)));
-  // integer thresholds, rounded so that passing them implies the double test:
-  // ghi(k) <= 0 <=> Cu_k <= (T - 2 dC - lam sm) / 2q;  glo(k) >= 0 <=> Cu_k >= (T + 2 dC - lam sp) / 2q
-  const double iq2 = 0.5 / q;
-  auto thr_le = [&](double x) -> long long {
-    x = x * iq2 * (1.0 - 0x1p-44) - 0x1p-8;
-    return x < 0.0 ? -1LL : (x >= 0x1p62 ? (1LL << 62) : (long long)floor(x));
-  };
-  auto thr_ge = [&](double x) -> long long {
-    x = x * iq2 * (1.0 + 0x1p-44) + 0x1p-8;
-    return x <= 0.0 ? 0LL : (x >= 0x1p62 ? (1LL << 62) : (long long)ceil(x));
-  };
-  const long long tLm = thr_le(T - 2.0 * dC + lam), tLp = thr_le(T - 2.0 * dC - lam);  // sm = -1 / +1
-  const long long tRm = thr_ge(T + 2.0 * dC + lam), tRp = thr_ge(T + 2.0 * dC - lam);  // sp = -1 / +1
-  // kL = last edge with ghi <= 0, kR = first with glo >= 0: Cu_k grows and
-  // the thresholds only drop at the sign change, so both tests are monotone
-  // in k and two binary searches over the prefix sums find them
-  const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
-  const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
-  const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
-  const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
-  auto pL = [&](int k) {
-    const unsigned cu = H.cu(k);
-    return k >= z1 ? (hasL_p & (cu <= uLp)) : (hasL_m & (cu <= uLm));
-  };
-  auto pR = [&](int k) {
-    const unsigned cu = H.cu(k);
-    return k >= z0 ? (hasR_p & (cu >= uRp)) : (hasR_m & (cu >= uRm));
-  };
-  int kL, kR;
-  {
-    int a = -1, b = kNI + 1;  // pL(a) holds, pL(b) fails
-    while (b - a > 1) {
-      const int mid = (a + b) >> 1;
-      if (pL(mid)) a = mid;
-      else b = mid;
-    }
-    kL = a;
-    a = -1;
-    b = kNI + 1;  // pR(a) fails, pR(b) holds
-    while (b - a > 1) {
-      const int mid = (a + b) >> 1;
-      if (pR(mid)) b = mid;
-      else a = mid;
-    }
-    kR = b;  // kNI + 1 = kNB - 1: not in the bracket
-  }
-  const long long CuL = kL >= 0 ? (long long)H.cu(kL) : 0, SCL = kL >= 0 ? (long long)H.sc(kL) : 0;
-  const long long CuR = kR <= kNI ? (long long)H.cu(kR) : 0, SCR = kR <= kNI ? (long long)H.sc(kR) : 0;
-  const long long CuC = H.cu(kc), SCC = (long long)H.sc(kc), CuC1 = H.cu(kc + 1), Cu0 = H.cu(0);
-  const long long Cu62 = H.cu(kNI), SC62 = (long long)H.sc(kNI);
-  const double q2 = 2.0 * q;
-  auto glo = [&](int k, long long Cu) { return q2 * (double)Cu - 2.0 * dC - T + (k >= z0 ? lam : -lam); };
-  auto ghi = [&](int k, long long Cu) { return q2 * (double)Cu + 2.0 * dC - T + (k >= z1 ? lam : -lam); };
-  auto Ilo = [&](int k, long long SC) {  // SP(k) = sum_{q<k} sp(q) = k - 2 min(k, z0)
-    return w * (q2 * (double)SC - (double)k * (2.0 * dC + T) + lam * (double)(k - 2 * min(k, z0)));
-  };
-  auto Ihi = [&](int k, long long SC, long long Cu) {  // SM1(k) = sum_{q=1..k} sm(q)
-    const int le = max(0, min(k, z1 - 1));
-    return w * (q2 * (double)(SC + Cu - Cu0) + (double)k * (2.0 * dC - T) + lam * (double)(k - 2 * le));
-  };
-  const double IloC = Ilo(kc, SCC), IhiC = Ihi(kc, SCC, CuC);
-  const double gloC = glo(kc, CuC), ghiC = ghi(kc + 1, CuC1), gloL = kL >= 0 ? glo(kL, CuL) : 0.0;
-  const double CL = q * (double)CuL, CR = kR <= kNI ? q * (double)CuR : T;
-  // f at e_kc from f(c), then at any edge k from e_kc
-  const double dc = c - edge(kc);
-  const double fkc_lo = fc - dc * ghiC, fkc_hi = fc - dc * gloC;
-  auto f_lo = [&](int k, long long SC, long long Cu) {
-    return k >= kc ? fkc_lo + (Ilo(k, SC) - IloC) : fkc_lo - (IhiC - Ihi(k, SC, Cu));
-  };
-  auto f_hi = [&](int k, long long SC, long long Cu) {
-    return k >= kc ? fkc_hi + (Ihi(k, SC, Cu) - IhiC) : fkc_hi - (IloC - Ilo(k, SC));
-  };
-  // f(0) = sum_i |x_ij|: the dead value; colsum carries the rounding of an
-  // n-term f64 sum (any order): within (n + 128) 2^-53 of it
-  const double f0e = (double)(n + 128) * 0x1p-53 * colsum;
-  const double f0 = colsum - f0e;  // a lower bound of f(0) (the kink bounds below)
-  double lb, ub = fmin(fc + eps, colsum + f0e);
-  const double eL = kL >= 0 ? edge(kL) : -INFINITY, eR = kR <= kNI ? edge(kR) : INFINITY;
-  if (kL >= 0 && kR <= kNI && kL <= kR) {
-    lb = f_lo(kL, SCL, CuL) - eps + fmin(0.0, gloL) * (eR - eL);
-    ub = fmin(ub, fmin(f_hi(kL, SCL, CuL), f_hi(kR, SCR, CuR)) + eps);
-  } else {
-    lb = 0.0;  // the optimum lies beyond the bracket: only the trivial bound
-    if (kL == kNI) ub = fmin(ub, f_hi(kNI, SC62, Cu62) + eps);
-  }
-  if (eL <= 0.0 && 0.0 <= eR) {
-    // the penalty's kink: g(0-) <= 2 W(r < eR) - T - lam, g(0+) >= 2 W(r < eL) - T + lam;
-    // f(v) >= f0 + g(0-) v on v <= 0 and f(v) >= f0 + g(0+) v on v >= 0
-    const double g0m = 2.0 * (CR + dC) - T - lam, g0p = 2.0 * ((kL >= 0 ? CL : 0.0) - dC) - T + lam;
-    const double left = isfinite(eL) ? f0 + fmax(0.0, g0m) * eL : (g0m <= 0.0 ? f0 : 0.0);
-    const double right = isfinite(eR) ? f0 + fmin(0.0, g0p) * eR : (g0p >= 0.0 ? f0 : 0.0);
-    lb = fmax(lb, fmin(left, right) - pert);
-  }
-  *lbo = fmax(0.0, lb);
-  *ubo = ub;
-  // where the optimum lies (seed for the exact solver), widened for the
-  // rows' float ratios and edges
-  if (kL >= 0 && kR <= kNI && kL <= kR) {
-    const double d = 0x1p-19 * (fabs(eL) + fabs(eR) + fabs(lo) + fabs(hi)) + 0x1p-10 * w;
-    *range = make_double2(eL - d, eR + d);
-  } else {
-    *range = make_double2(-INFINITY, INFINITY);
-  }
-  // the next pass's range: between the edges where the optimum provably lies
-  // (a little wider), or, when a side is not in the bracket, extended there
-  const float flo = (float)lo, fhi = (float)hi, span = fhi - flo;
-  float a, b;
-  if (kL >= 0 && kR <= kNI) {
-    a = (float)edge(max(0, min(kL, kR - 1)));
-    b = (float)edge(min(kNI, max(kR, kL + 1)));
-  } else if (kR <= kNI) {  // optimum at or below lo
-    a = fminf(smin, flo) - 2.f * span;
-    b = (float)edge(kR);
-  } else if (kL >= 0) {  // at or above the last edge
-    a = (float)edge(kL);
-    b = fmaxf(smax, fhi) + 2.f * span;
-  } else {  // no edge is decisive (margins dominate): keep the range
-    a = flo;
-    b = fhi;
-  }
-  const float mg = 0.05f * (b - a);
-  a -= mg;
-  b += mg;
-  if (!(b > a)) b = a + fmaxf(fabsf(a), 1e-30f) * 1e-6f;
-  *next = make_float2(a, b);
+  ColumnBounds(H, q, lo, hi, c, ec, T, colsum, n).at(lam, smin, smax, lbo, ubo, range, next);
 }
 
 // Sample bracket of one problem: float ratios of 32 strided rows, sorted in
@@ -509,6 +538,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   __shared__ unsigned done[kBStages];      // warps finished with the stage's chunk
   __shared__ float sbr[5][kBProb];         // problem q: (lo, hi, cen, smin, smax)
   __shared__ unsigned long long psum[kBWarps][2];  // per-warp pivot sums (lb, ub)
+  __shared__ unsigned long long psumg[MULTI ? kBWarps : 1][kBLamGroup][2];  // the same per penalty group
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int th = warp % kBTH, rg = warp / kBTH;
   const int64_t n = P.n, m = P.m, np = P.np;
@@ -728,6 +758,43 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     }
     __syncthreads();
   };
+  // the same for kBLamGroup penalties at once (multi-penalty passes): one
+  // pair of barriers per group instead of per penalty
+  auto pivot_sums_group = [&](const double* lb, const double* ub, int l0) {
+    unsigned long long ql[kBLamGroup], qu[kBLamGroup];
+#pragma unroll
+    for (int g = 0; g < kBLamGroup; ++g) {
+      ql[g] = (unsigned long long)__double2ull_rd(ldexp(lb[g], fx));
+      qu[g] = (unsigned long long)__double2ull_ru(ldexp(ub[g], fx));
+      for (int o = 16; o; o >>= 1) {
+        ql[g] += __shfl_xor_sync(0xffffffffu, ql[g], o);
+        qu[g] += __shfl_xor_sync(0xffffffffu, qu[g], o);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < kBLamGroup; ++g) {
+        psumg[warp][g][0] = ql[g];
+        psumg[warp][g][1] = qu[g];
+      }
+    }
+    __syncthreads();
+    constexpr int WP = kBWarps / kBPiv;
+    if (tid < kBPiv * kBLamGroup) {
+      const int t = tid / kBLamGroup, g = tid % kBLamGroup;
+      const int64_t k = (int64_t)blockIdx.y * kBPiv + t;
+      if (k < P.npiv && l0 + g < P.nlam) {
+        unsigned long long sl = 0, su = 0;
+        for (int w = t * WP; w < (t + 1) * WP; ++w) {
+          sl += psumg[w][g][0];
+          su += psumg[w][g][1];
+        }
+        atomicAdd(&P.LBq[(int64_t)(l0 + g) * P.npiv + k], sl);
+        atomicAdd(&P.UBq[(int64_t)(l0 + g) * P.npiv + k], su);
+      }
+    }
+    __syncthreads();
+  };
   int64_t pv;
   bool okk, dg;
   double T, u;
@@ -746,21 +813,30 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   if (MULTI) {
     Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
     H.build();  // once for every penalty
-    for (int l = 0; l < P.nlam; ++l) {
-      double lb = 0.0, ub = 0.0;
-      float2 nx = make_float2(tlo, thi);
-      if (live) {
-        double2 rg2;
-        column_bounds(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u, P.lams[l],
-                      P.colsum[qj], n, sbr[3][tid], sbr[4][tid], &lb, &ub, &rg2, &nx);
-        ub = fmin(ub, P.colsum[qj] * (1.0 + 0x1p-20));
-        lb = fmin(lb, ub);
-      } else if (okk && qj < m && dg) {
-        lb = ub = P.colsum[qj];  // fit.py:66-72: v = 0, error = sum |x|
+    const ColumnBounds CB(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u,
+                          live ? P.colsum[qj] : 0.0, n);
+    for (int l0 = 0; l0 < P.nlam; l0 += kBLamGroup) {
+      double lbg[kBLamGroup], ubg[kBLamGroup];
+#pragma unroll
+      for (int g = 0; g < kBLamGroup; ++g) {
+        const int l = l0 + g;
+        double lb = 0.0, ub = 0.0;
+        if (l < P.nlam) {
+          float2 nx = make_float2(tlo, thi);
+          if (live) {
+            CB.at(P.lams[l], sbr[3][tid], sbr[4][tid], &lb, &ub, nullptr, &nx);
+            ub = fmin(ub, P.colsum[qj] * (1.0 + 0x1p-20));
+            lb = fmin(lb, ub);
+          } else if (okk && qj < m && dg) {
+            lb = ub = P.colsum[qj];  // fit.py:66-72: v = 0, error = sum |x|
+          }
+          // each penalty's next range, for a continuing pass per (penalty, pivot) entry
+          if (P.NEXTm && okk && qj < m) P.NEXTm[((int64_t)l * P.npiv + qk) * m + qj] = nx;
+        }
+        lbg[g] = lb;
+        ubg[g] = ub;
       }
-      // each penalty's next range, for a continuing pass per (penalty, pivot) entry
-      if (P.NEXTm && okk && qj < m) P.NEXTm[((int64_t)l * P.npiv + qk) * m + qj] = nx;
-      pivot_sums(lb, ub, l);
+      pivot_sums_group(lbg, ubg, l0);
     }
     return;
   }
