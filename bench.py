@@ -180,6 +180,9 @@ def cpu_reference(X, lams, budget_s: float, threads: int | None = None):
     solves = done * (m - 1) * len(lams)
     per_fit = dt * m / done / len(lams)
     what = "l1line.fit_for_pivot (baseline/_ref)" if ref is not None else "oracle C port"
+    if ref is None and len(lams) > 1:
+        what += (" (one tableau per pivot shared by every penalty: faster than the reference's one fit_line "
+                 "per penalty)")
     return (solves / dt, per_fit, f"{what}: {done}/{m} pivots (evenly spread) x {len(lams)} lambda of the same "
             f"input on {threads} threads, {dt:.1f}s", "reference" if ref is not None else "port")
 
