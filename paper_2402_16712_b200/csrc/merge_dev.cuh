@@ -238,9 +238,12 @@ __global__ void __launch_bounds__(kMrgThreads) k_mrg_intervals(
       }
       const double blo = fmax(fmax(blo4[0], blo4[1]), fmax(blo4[2], blo4[3]));
       const double bhi = fmin(fmin(bhi4[0], bhi4[1]), fmin(bhi4[2], bhi4[3]));
-      if (!dom) {
-        if (0.0 < blo && blo < bhi && __dadd_rn(lam_k, blo) <= lam_next) st[atomicAdd(&nst, 1)] = __dadd_rn(lam_k, blo);
-        else if (blo <= 0.0 && 0.0 < bhi) st[atomicAdd(&nst, 1)] = lam_k;
+      // starts within DEDUP_TOL of lam_k (the elif branch's lam_k itself, always)
+      // or of lam_next never survive the dedup walk below -- the sorted walk
+      // drops them whatever else is kept -- so only the others are collected
+      if (!dom && 0.0 < blo && blo < bhi) {
+        const double b0 = __dadd_rn(lam_k, blo);
+        if (b0 <= lam_next && __dsub_rn(b0, lam_k) > 1e-9 && __dsub_rn(lam_next, b0) > 1e-9) st[atomicAdd(&nst, 1)] = b0;
       }
     }
     __syncthreads();
