@@ -633,23 +633,46 @@ int l1b_snap_events(const double* lambdas, int64_t K, const double* bp, int64_t 
   std::vector<uint64_t> key(E);
   std::vector<int64_t> idx(E), tmp_i(E);
   std::vector<uint64_t> tmp_k(E);
-  for (int64_t e = 0; e < E; ++e) {
-    uint64_t b;
-    const double x = bp[e] == 0.0 ? 0.0 : bp[e];  // -0.0 sorts with +0.0
-    std::memcpy(&b, &x, 8);
-    key[e] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving image of the double
-    idx[e] = e;
-  }
-  for (int pass = 0; pass < 4; ++pass) {  // 16-bit digits, stable
-    const int sh = 16 * pass;
-    std::vector<int64_t> cnt(65537, 0);
-    for (int64_t e = 0; e < E; ++e) ++cnt[((key[e] >> sh) & 0xffff) + 1];
-    for (int b = 0; b < 65536; ++b) cnt[b + 1] += cnt[b];
-    for (int64_t e = 0; e < E; ++e) {
-      const int64_t at = cnt[(key[e] >> sh) & 0xffff]++;
-      tmp_k[at] = key[e];
-      tmp_i[at] = idx[e];
+  const int NT = (int)std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), E / 65536));
+  auto par = [&](auto&& fn) {  // fn(t, lo, hi) over NT contiguous slices of [0, E)
+    std::vector<std::thread> th;
+    for (int t = 0; t < NT; ++t) th.emplace_back([&, t] { fn(t, E * t / NT, E * (t + 1) / NT); });
+    for (auto& x : th) x.join();
+  };
+  par([&](int, int64_t lo, int64_t hi) {
+    for (int64_t e = lo; e < hi; ++e) {
+      uint64_t b;
+      const double x = bp[e] == 0.0 ? 0.0 : bp[e];  // -0.0 sorts with +0.0
+      std::memcpy(&b, &x, 8);
+      key[e] = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // order-preserving image of the double
+      idx[e] = e;
     }
+  });
+  // LSD radix sort, 16-bit digits, stable; each pass: per-slice digit counts,
+  // an exclusive scan over (digit, slice), parallel scatter
+  std::vector<int64_t> cnt((size_t)NT * 65536);
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 16 * pass;
+    std::fill(cnt.begin(), cnt.end(), 0);
+    par([&](int t, int64_t lo, int64_t hi) {
+      int64_t* c = cnt.data() + (size_t)t * 65536;
+      for (int64_t e = lo; e < hi; ++e) ++c[(key[e] >> sh) & 0xffff];
+    });
+    int64_t run = 0;
+    for (int d = 0; d < 65536; ++d)
+      for (int t = 0; t < NT; ++t) {
+        const int64_t v = cnt[(size_t)t * 65536 + d];
+        cnt[(size_t)t * 65536 + d] = run;
+        run += v;
+      }
+    par([&](int t, int64_t lo, int64_t hi) {
+      int64_t* c = cnt.data() + (size_t)t * 65536;
+      for (int64_t e = lo; e < hi; ++e) {
+        const int64_t at = c[(key[e] >> sh) & 0xffff]++;
+        tmp_k[at] = key[e];
+        tmp_i[at] = idx[e];
+      }
+    });
     key.swap(tmp_k);
     idx.swap(tmp_i);
   }
