@@ -473,6 +473,8 @@ def run_ours(args):
         for t in range(ncomp):
             if ncomp > 1 and eng.absmax() <= 1e-10 * scale:
                 break
+            if ncomp > 1:  # fit_subspace's steering policy (api.fit_subspace)
+                eng.set_steer(0 if t == 0 else -1)
             wins = eng.shard_winners(lams, p_begin, p_stride, npiv, ub_exchange=ex)
             if world > 1:
                 wins = combine_winners(wins, m)

@@ -316,6 +316,13 @@ int l1b_merge_path(const double* X, int64_t n, int64_t m, const double* lambdas,
  * segments come back in one malloc'ed block *o_seg of [count][8 + m]
  * doubles (lo, hi, pivot, err, pen, obj, z_lo, z_hi, v[m]); free it with
  * l1b_csv_free. */
+/* Steering of l1b_fit_line's first bound pass on workspace d_ws: -1
+ * automatic (a 1-in-8 row-chunk steering pass for n >= 32768), 0 off, s > 1 a
+ * steering pass over every s-th 64-row chunk.  fit_subspace turns it off for
+ * the first component (one pass prunes it) and back to automatic for the
+ * deflated ones (whose pivots sit within ~1e-4 of each other). */
+int l1b_set_steer(const void* d_ws, int32_t mode);
+
 /* path.py:157-163 for E breakpoint events at once: out_order[E] = the events
  * grouped by their snapped grid index (ascending; insertion order within a
  * group), out_off[K+1] = group offsets.  Host arrays.  L1B_EINTERNAL when a

@@ -50,6 +50,7 @@ ABI_SYMBOLS = (
     "l1b_merge_path",
     "l1b_merge_path_device",
     "l1b_snap_events",
+    "l1b_set_steer",
     "l1b_brute_force_columns",
     "l1b_last_bound_ms",
     "l1b_atoms_probe",
@@ -167,6 +168,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_merge_path_device.restype = ctypes.c_int
     lib.l1b_merge_path_device.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
                                           ctypes.POINTER(ctypes.c_void_p), _vp, _vp, _sz, _vp]
+    lib.l1b_set_steer.restype = ctypes.c_int
+    lib.l1b_set_steer.argtypes = [_vp, _i32]
     lib.l1b_snap_events.restype = ctypes.c_int
     lib.l1b_snap_events.argtypes = [_vp, _i64, _vp, _i64, ctypes.c_double, _vp, _vp]
     lib.l1b_brute_force_columns.restype = ctypes.c_int

@@ -185,6 +185,10 @@ def fit_subspace(data, lam: float, k: int, threads: int | None = None) -> Subspa
     for t in range(k):
         if eng.absmax() <= 1e-10 * scale:
             return SubspaceFit(tuple(comps), degenerate=True)
+        # the raw data's pivots are far apart: one unsteered pass prunes them;
+        # deflated components' pivots sit within ~1e-4 of each other and need
+        # the steering pass of tall data
+        eng.set_steer(0 if t == 0 else -1)
         line = _line(eng.shard_winners([float(lam)])[0])
         comps.append(line)
         # subspace.py:75 deflates after every component, the last one too, and

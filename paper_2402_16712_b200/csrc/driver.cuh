@@ -89,6 +89,11 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
     // tall columns: a steering pass over a row sample narrows the first full
     // pass's brackets (deflated components of tall data prune only then)
     int steer = n >= kSteerRows ? kSteerStride : 0;
+    {
+      std::lock_guard<std::mutex> g(g_win_mu);
+      const auto it = g_steer.find(d_ws);
+      if (it != g_steer.end() && it->second >= 0) steer = it->second;  // l1b_set_steer
+    }
     if (const char* e = getenv("L1B200_STEER")) steer = atoi(e);  // tuning knob: chunk stride, 0 = off
     st = fit_impl(d_X, n, m, &lam, 1, p_begin, p_stride, nullptr, npiv, true, nullptr, nullptr, nullptr, nullptr,
                   d_lb, d_ub, d_ws, ws_bytes, stream, 1, nullptr, 0, nullptr, nullptr, nullptr, /*lean=*/true, steer);

@@ -199,6 +199,7 @@ def fit_subspace_distributed(data, lam: float, k: int, group=None):
     for t in range(k):
         if eng.absmax() <= 1e-10 * scale:
             return SubspaceFit(tuple(comps), degenerate=True)
+        eng.set_steer(0 if t == 0 else -1)  # api.fit_subspace's steering policy
         local = _shard_solve(eng, [float(lam)], p_begin, p_stride, npiv, eng.auto_prune(), group)
         w = combine_winners(local, m, group)[0]
         comps.append(FittedLine(v=w.v, preserved=w.pivot, lam=w.lam, error=w.error,

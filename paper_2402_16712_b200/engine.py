@@ -194,6 +194,10 @@ class DeviceFit:
                                             self.tmp.data_ptr(), self._s), "l1b_deflate")
         self.prepare()
 
+    def set_steer(self, mode: int) -> None:
+        """Steering of the first bound pass (l1b_set_steer): -1 automatic, 0 off, s > 1 stride."""
+        _lib.check(self.lib.l1b_set_steer(self.ws.data_ptr(), int(mode)), "l1b_set_steer")
+
     def absmax(self) -> float:
         with torch.cuda.device(self.device):
             _lib.check(self.lib.l1b_absmax(self.X.data_ptr(), self.n, self.m, self.scalar.data_ptr(),
