@@ -184,3 +184,29 @@ def test_discordance_and_l0_fraction():
         l1b.discordance([0.0, 0.0], [1.0, 0.0])
     with pytest.raises(ValueError):
         l1b.l0_fraction(v, tol=-1.0)
+
+
+def test_pivot_events_equal_breakpoint_maps():
+    """path._pivot_events (solution_path's array route) yields exactly the entries
+    of path._maps (pivot_breakpoints' tuples, path.py:76-102) in the same order:
+    live runs clamped at 0, the death entry last among equal weights, dead runs dropped."""
+    from paper_2402_16712_b200 import path as P
+
+    rng = np.random.default_rng(11)
+    for trial in range(30):
+        m, k = int(rng.integers(2, 7)), int(rng.integers(1, 12))
+        p = int(rng.integers(m))
+        rs = np.round(rng.normal(size=(m - 1, k)), 1)
+        st = np.round(rng.normal(size=(m - 1, k)) * 3, 0)           # ties and zeros in the starts
+        rt = st + 2.0 * np.abs(np.round(rng.normal(size=(m - 1, k)), 0))
+        rt[rng.random(rt.shape) < 0.3] = -1.0                       # dead runs
+
+        class Eng:
+            def pivot_runs(self, pivot):
+                return rs, st, rt
+        Eng.m = m
+        tgt, w, v = P._pivot_events(Eng(), p)
+        maps = P._maps(p, m, rs, st, rt)
+        want = [(t, bp, val) for t, entries in maps.entries.items() for bp, val in entries]
+        got = list(zip(tgt.tolist(), w.tolist(), v.tolist()))
+        assert got == want, trial
