@@ -97,9 +97,16 @@ struct Prefix {
     }
   }
   __device__ __forceinline__ unsigned cu(int k) const { return h[k * hs]; }
+  // static indices only (a select chain and predicated loads): the struct stays
+  // in registers, so h keeps its address space (shared loads, no stack frame)
   __device__ __forceinline__ unsigned long long sc(int k) const {
-    unsigned long long s = sc8[k >> 3];
-    for (int q = k & ~7; q < k; ++q) s += h[q * hs];
+    const int b = k >> 3, q0 = k & ~7;
+    unsigned long long s = sc8[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s = b == i ? sc8[i] : s;
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+      if (q0 + d < k) s += h[(q0 + d) * hs];
     return s;
   }
 };
@@ -165,23 +172,18 @@ struct ColumnBounds {
     const double fc = ec + lam * fabs(c);
     // integer thresholds, rounded so that passing them implies the double test:
     // ghi(k) <= 0 <=> Cu_k <= (T - 2 dC - lam sm) / 2q;  glo(k) >= 0 <=> Cu_k >= (T + 2 dC - lam sp) / 2q
-    auto thr_le = [&](double x) -> long long {
-      x = x * iq2 * (1.0 - 0x1p-44) - 0x1p-8;
-      return x < 0.0 ? -1LL : (x >= 0x1p62 ? (1LL << 62) : (long long)floor(x));
-    };
-    auto thr_ge = [&](double x) -> long long {
-      x = x * iq2 * (1.0 + 0x1p-44) + 0x1p-8;
-      return x <= 0.0 ? 0LL : (x >= 0x1p62 ? (1LL << 62) : (long long)ceil(x));
-    };
-    const long long tLm = thr_le(T - 2.0 * dC + lam), tLp = thr_le(T - 2.0 * dC - lam);  // sm = -1 / +1
-    const long long tRm = thr_ge(T + 2.0 * dC + lam), tRp = thr_ge(T + 2.0 * dC - lam);  // sp = -1 / +1
+    // (Cu_k < 2^32: a threshold is "none pass" / "all pass" outside [0, 2^32 - 1])
+    auto xle = [&](double x) { return x * iq2 * (1.0 - 0x1p-44) - 0x1p-8; };
+    auto xge = [&](double x) { return x * iq2 * (1.0 + 0x1p-44) + 0x1p-8; };
+    const double xLm = xle(T - 2.0 * dC + lam), xLp = xle(T - 2.0 * dC - lam);  // sm = -1 / +1
+    const double xRm = xge(T + 2.0 * dC + lam), xRp = xge(T + 2.0 * dC - lam);  // sp = -1 / +1
     // kL = last edge with ghi <= 0, kR = first with glo >= 0: Cu_k grows and
     // the thresholds only drop at the sign change, so both tests are monotone
-    // in k and two binary searches over the prefix sums find them
-    const bool hasL_m = tLm >= 0, hasL_p = tLp >= 0;
-    const unsigned uLm = (unsigned)min(max(tLm, 0LL), 0xffffffffLL), uLp = (unsigned)min(max(tLp, 0LL), 0xffffffffLL);
-    const unsigned uRm = (unsigned)min(tRm, 0xffffffffLL), uRp = (unsigned)min(tRp, 0xffffffffLL);
-    const bool hasR_m = tRm <= 0xffffffffLL, hasR_p = tRp <= 0xffffffffLL;
+    // in k and two bisections over the prefix sums find them
+    const bool hasL_m = xLm >= 0.0, hasL_p = xLp >= 0.0;
+    const unsigned uLm = __double2uint_rd(fmin(xLm, 4294967295.0)), uLp = __double2uint_rd(fmin(xLp, 4294967295.0));
+    const bool hasR_m = xRm <= 4294967295.0, hasR_p = xRp <= 4294967295.0;
+    const unsigned uRm = __double2uint_ru(fmax(xRm, 0.0)), uRp = __double2uint_ru(fmax(xRp, 0.0));
     auto pL = [&](int k) {
       const unsigned cu = H.cu(k);
       return k >= z1 ? (hasL_p & (cu <= uLp)) : (hasL_m & (cu <= uLm));
@@ -190,24 +192,17 @@ struct ColumnBounds {
       const unsigned cu = H.cu(k);
       return k >= z0 ? (hasR_p & (cu >= uRp)) : (hasR_m & (cu >= uRm));
     };
-    int kL, kR;
-    {
-      int a = -1, b = kNI + 1;  // pL(a) holds, pL(b) fails
-      while (b - a > 1) {
-        const int mid = (a + b) >> 1;
-        if (pL(mid)) a = mid;
-        else b = mid;
-      }
-      kL = a;
-      a = -1;
-      b = kNI + 1;  // pR(a) fails, pR(b) holds
-      while (b - a > 1) {
-        const int mid = (a + b) >> 1;
-        if (pR(mid)) b = mid;
-        else a = mid;
-      }
-      kR = b;  // kNI + 1 = kNB - 1: not in the bracket
+    // fixed six-step bisections over edges 0..62 (branch-free): kL in [-1, 62]
+    // (pL holds up to it), kR in [0, 63] (pR holds from it; 63 = kNI + 1: not
+    // in the bracket)
+    static_assert(kNI + 1 == 63, "six steps cover edges -1..62");
+    int kL = -1, kR = -1;
+#pragma unroll
+    for (int st = 32; st; st >>= 1) {
+      kL = pL(kL + st) ? kL + st : kL;
+      kR = pR(kR + st) ? kR : kR + st;
     }
+    ++kR;
     const long long CuL = kL >= 0 ? (long long)H.cu(kL) : 0, SCL = kL >= 0 ? (long long)H.sc(kL) : 0;
     const long long CuR = kR <= kNI ? (long long)H.cu(kR) : 0, SCR = kR <= kNI ? (long long)H.sc(kR) : 0;
     auto glo = [&](int k, long long Cu) { return q2 * (double)Cu - 2.0 * dC - T + (k >= z0 ? lam : -lam); };
@@ -720,6 +715,14 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     for (int ee = 0; ee < kBTE; ++ee) ecx[rg * kBProb + t * kBTgt + (th * kBTE + ee) * 32 + lane] = ec[t][ee];
   __syncthreads();
   const int fx = P.fxk ? *P.fxk : 0;
+  // x 2^fx as one multiply (exact for normal results, as ldexp; an upper
+  // bound whose scaled value underflows still rounds up to 1)
+  const double fxs = ldexp(1.0, fx);
+  auto fx_down = [&](double x) { return (unsigned long long)__double2ull_rd(x * fxs); };
+  auto fx_up = [&](double x) {
+    const unsigned long long r = __double2ull_ru(x * fxs);
+    return (unsigned long long)(r == 0ull && x > 0.0 ? 1ull : r);
+  };
   double ect = 0.0;
 #pragma unroll
   for (int g = 0; g < kBRG; ++g) ect += ecx[g * kBProb + tid];
@@ -731,8 +734,8 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   auto pivot_sums = [&](double lb, double ub, int64_t row) {
     unsigned long long ql = 0, qu = 0;
     if (P.LBq) {
-      ql = (unsigned long long)__double2ull_rd(ldexp(lb, fx));
-      qu = (unsigned long long)__double2ull_ru(ldexp(ub, fx));
+      ql = fx_down(lb);
+      qu = fx_up(ub);
     }
     for (int o = 16; o; o >>= 1) {
       ql += __shfl_xor_sync(0xffffffffu, ql, o);
@@ -761,22 +764,33 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   // the same for kBLamGroup penalties at once (multi-penalty passes): one
   // pair of barriers per group instead of per penalty
   auto pivot_sums_group = [&](const double* lb, const double* ub, int l0) {
+    static_assert(kBLamGroup == 4, "transposed reduction below");
     unsigned long long ql[kBLamGroup], qu[kBLamGroup];
 #pragma unroll
     for (int g = 0; g < kBLamGroup; ++g) {
-      ql[g] = (unsigned long long)__double2ull_rd(ldexp(lb[g], fx));
-      qu[g] = (unsigned long long)__double2ull_ru(ldexp(ub[g], fx));
-      for (int o = 16; o; o >>= 1) {
-        ql[g] += __shfl_xor_sync(0xffffffffu, ql[g], o);
-        qu[g] += __shfl_xor_sync(0xffffffffu, qu[g], o);
-      }
+      ql[g] = fx_down(lb[g]);
+      qu[g] = fx_up(ub[g]);
     }
-    if (lane == 0) {
+    // transposed butterfly: each exchange halves the penalties a lane keeps,
+    // so lane 8g + (any of 0..7) ends with penalty g's warp sum (6 exchanges
+    // per quantity instead of 4 x 5; integer sums, order-free)
+    const bool b4 = lane & 16, b3 = lane & 8;
+    unsigned long long wl[2], wu[2];
 #pragma unroll
-      for (int g = 0; g < kBLamGroup; ++g) {
-        psumg[warp][g][0] = ql[g];
-        psumg[warp][g][1] = qu[g];
-      }
+    for (int j = 0; j < 2; ++j) {
+      wl[j] = (b4 ? ql[2 + j] : ql[j]) + __shfl_xor_sync(0xffffffffu, b4 ? ql[j] : ql[2 + j], 16);
+      wu[j] = (b4 ? qu[2 + j] : qu[j]) + __shfl_xor_sync(0xffffffffu, b4 ? qu[j] : qu[2 + j], 16);
+    }
+    unsigned long long sl = (b3 ? wl[1] : wl[0]) + __shfl_xor_sync(0xffffffffu, b3 ? wl[0] : wl[1], 8);
+    unsigned long long su = (b3 ? wu[1] : wu[0]) + __shfl_xor_sync(0xffffffffu, b3 ? wu[0] : wu[1], 8);
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+      sl += __shfl_xor_sync(0xffffffffu, sl, o);
+      su += __shfl_xor_sync(0xffffffffu, su, o);
+    }
+    if ((lane & 7) == 0) {
+      psumg[warp][lane >> 3][0] = sl;
+      psumg[warp][lane >> 3][1] = su;
     }
     __syncthreads();
     constexpr int WP = kBWarps / kBPiv;
@@ -813,8 +827,13 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   if (MULTI) {
     Prefix H{hist + qt * kNB * kBTgt + qs, kBTgt};
     H.build();  // once for every penalty
-    const ColumnBounds CB(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u,
-                          live ? P.colsum[qj] : 0.0, n);
+    // penalty-invariant per column: loaded once, not per penalty (the stores
+    // below could alias them as far as the compiler knows)
+    const double csj = okk && qj < m ? P.colsum[qj] : 0.0;
+    const float smn = sbr[3][tid], smx = sbr[4][tid];
+    float2* nxp = P.NEXTm && okk && qj < m ? P.NEXTm + qk * m + qj : nullptr;
+    const int64_t nxs = P.npiv * m;
+    const ColumnBounds CB(H, ldexp(u, 21), (double)tlo, (double)thi, (double)tcf, ect, T * u, live ? csj : 0.0, n);
     for (int l0 = 0; l0 < P.nlam; l0 += kBLamGroup) {
       double lbg[kBLamGroup], ubg[kBLamGroup];
 #pragma unroll
@@ -824,14 +843,14 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
         if (l < P.nlam) {
           float2 nx = make_float2(tlo, thi);
           if (live) {
-            CB.at(P.lams[l], sbr[3][tid], sbr[4][tid], &lb, &ub, nullptr, &nx);
-            ub = fmin(ub, P.colsum[qj] * (1.0 + 0x1p-20));
+            CB.at(P.lams[l], smn, smx, &lb, &ub, nullptr, &nx);
+            ub = fmin(ub, csj * (1.0 + 0x1p-20));
             lb = fmin(lb, ub);
-          } else if (okk && qj < m && dg) {
-            lb = ub = P.colsum[qj];  // fit.py:66-72: v = 0, error = sum |x|
+          } else if (dg) {
+            lb = ub = csj;  // fit.py:66-72: v = 0, error = sum |x| (0 past the last target)
           }
           // each penalty's next range, for a continuing pass per (penalty, pivot) entry
-          if (P.NEXTm && okk && qj < m) P.NEXTm[((int64_t)l * P.npiv + qk) * m + qj] = nx;
+          if (nxp) nxp[l * nxs] = nx;
         }
         lbg[g] = lb;
         ubg[g] = ub;
