@@ -174,6 +174,11 @@ int l1b_deflate(double* d_X, int64_t n, int64_t m, const double* d_v, double* d_
 /* max_ij |x_ij| into d_out[0] (the early-stop test of subspace.py:67,71). */
 int l1b_absmax(const double* d_X, int64_t n, int64_t m, double* d_out, void* stream);
 
+/* The same max_ij |x_ij| of the matrix the workspace was last prepared for
+ * (l1b_prepare computes it with the column statistics): one 8-byte copy into
+ * d_out[0] on the stream, no pass over X. */
+int l1b_prepared_absmax(const void* d_ws, int64_t n, int64_t m, size_t ws_bytes, double* d_out, void* stream);
+
 /* Self-test of the bit-exact division used by K1 (no reference counterpart;
  * it backs the parity claim for ratios.py:119 R = X[rows,t] / x_p): n_pairs
  * random (a, b) in the SAFE exponent window, counting results that differ

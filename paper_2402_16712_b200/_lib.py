@@ -28,6 +28,7 @@ ABI_SYMBOLS = (
     "l1b_residual_exact",
     "l1b_deflate",
     "l1b_absmax",
+    "l1b_prepared_absmax",
     "l1b_selftest_divide",
     "l1b_kernel_launches",
     "l1b_dfma_probe",
@@ -117,6 +118,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_deflate.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
     lib.l1b_absmax.restype = ctypes.c_int
     lib.l1b_absmax.argtypes = [_vp, _i64, _i64, _vp, _vp]
+    lib.l1b_prepared_absmax.restype = ctypes.c_int
+    lib.l1b_prepared_absmax.argtypes = [_vp, _i64, _i64, ctypes.c_size_t, _vp, _vp]
     lib.l1b_selftest_divide.restype = ctypes.c_int
     lib.l1b_selftest_divide.argtypes = [ctypes.c_uint64, _i64, _vp, _vp]
     lib.l1b_kernel_launches.restype = ctypes.c_uint64

@@ -54,13 +54,13 @@ constexpr int kBMinBlocks = kBTgt == 64 ? 2 : 1;
 #endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
 constexpr int kBRowsW = kBRows / kBRG;     // rows per warp per chunk
-constexpr int kBTile = kBRows * kBTgt * 4;  // the rows' x_ij of the CTA's targets (k_tile_q order)
+constexpr int kBTile = kBRows * kBTgt * 4;  // the rows' x_ij of the CTA's targets (k_tile's xq order)
 constexpr int kBPlane = kBRows * kBPiv * 12;  // k_group_bound records: 48 B per row
 constexpr int kBStage = kBTile + kBPlane;
 constexpr int kBStages = KB_STAGES;
 constexpr int kBHist = kBPiv * kNB * kBTgt * 4;  // [pivot][bin][target slot], exact 32-bit sums
 static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
-static_assert(kBTgt == 64 || kBTgt == 128, "k_tile_q lays out 64- or 128-target groups");
+static_assert(kBTgt == 64 || kBTgt == 128, "k_tile lays out 64- or 128-target groups");
 static_assert(kBRowsW % 2 == 0 && kBRows % kBRG == 0, "a warp takes whole row pairs of a chunk");
 static_assert(KB_FLUSH * kBRowsW <= 32, "residual summation margin (column_bounds) covers 16 row pairs");
 static_assert(kBStages * kBStage >= kBRG * kBProb * 8, "stage buffers hold the warps' residual shares");

@@ -66,13 +66,14 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
   double* d_err = w.drv + 2 * cap;
   double* d_pen = w.drv + 3 * cap;
   double* d_obj = w.drv + 4 * cap;
-  // n m max|x|: the re-score window's absolute floor
-  int st = l1b_absmax(d_X, n, m, d_err, stream);
-  if (st != L1B_OK) return st;
-  double amax = 0.0;
-  if (cudaMemcpyAsync(&amax, d_err, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
-    return L1B_ECUDA;
-  const double abs_scale = amax * (double)n * (double)m;
+  // n m max|x|: the re-score window's absolute floor (K0 left max |x| in the
+  // workspace; read with the first results, so nothing waits before the
+  // first pass is queued)
+  int st = L1B_OK;
+  double amax = 0.0, abs_scale = 0.0;  // abs_scale set once the copy has synchronised
+  auto read_amax = [&]() {
+    return cudaMemcpyAsync(&amax, w.flags + 6, sizeof(double), cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  };
   auto thr = [&](double top) {
     return std::isfinite(top) ? top + kPruneRtol * fabs(top) + kRescoreAtol * abs_scale : INFINITY;
   };
@@ -98,9 +99,11 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
     st = fit_impl(d_X, n, m, &lam, 1, p_begin, p_stride, nullptr, npiv, true, nullptr, nullptr, nullptr, nullptr,
                   d_lb, d_ub, d_ws, ws_bytes, stream, 1, nullptr, 0, nullptr, nullptr, nullptr, /*lean=*/true, steer);
     if (st != L1B_OK) return st;
-    if (cudaMemcpyAsync(lb.data(), d_lb, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    if (!read_amax() ||
+        cudaMemcpyAsync(lb.data(), d_lb, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaMemcpyAsync(ub.data(), d_ub, sizeof(double) * npiv, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
       return L1B_ECUDA;
+    abs_scale = amax * (double)n * (double)m;
     double top = INFINITY;
     for (double u : ub) top = std::min(top, u);  // NaN never wins std::min here
     if (ub_exchange) top = ub_exchange(top, exchange_ctx);  // the best upper bound over every shard
@@ -154,8 +157,10 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
   if (st != L1B_OK) return st;
   if (h_candidates) *h_candidates = nfit;
   std::vector<double> obj(nfit);
-  if (cudaMemcpyAsync(obj.data(), d_obj, sizeof(double) * nfit, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
+  if ((!do_prune && !read_amax()) ||
+      cudaMemcpyAsync(obj.data(), d_obj, sizeof(double) * nfit, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
     return L1B_ECUDA;
+  abs_scale = amax * (double)n * (double)m;
   // near-minimal candidates (engine._candidates), ascending pivot order
   double best = INFINITY;
   for (double o : obj) {

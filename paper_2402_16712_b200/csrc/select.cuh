@@ -43,7 +43,7 @@ constexpr double kBig = 1.7976931348623157e308;  // DBL_MAX: open window side
 struct SelParams {
   const double* Xt;      // X in 32-column tiles: ((j/32)*np + i)*32 + j%32
   const float* Xft;      // float copy of Xt
-  const float* Xq;       // k_bound's 128-target tiles (k_tile_q)
+  const float* Xq;       // k_bound's target-group tiles (k_tile's xq)
   const double2* gbw;    // shard (x_ip, wq_ip) records in 8-pivot groups: (g*np + i)*8 + w
   const float2* gpf;     // shard (float y_ip, float x_ip) in 8-pivot groups
   const unsigned* gwu;   // shard wq_ip / 2^21 (rounded) in 8-pivot groups

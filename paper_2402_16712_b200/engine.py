@@ -199,9 +199,10 @@ class DeviceFit:
         _lib.check(self.lib.l1b_set_steer(self.ws.data_ptr(), int(mode)), "l1b_set_steer")
 
     def absmax(self) -> float:
+        """max |x| of the prepared X (K0 computes it; no pass over X here)."""
         with torch.cuda.device(self.device):
-            _lib.check(self.lib.l1b_absmax(self.X.data_ptr(), self.n, self.m, self.scalar.data_ptr(),
-                                           self._s), "l1b_absmax")
+            _lib.check(self.lib.l1b_prepared_absmax(self.ws.data_ptr(), self.n, self.m, self.ws.numel(),
+                                                    self.scalar.data_ptr(), self._s), "l1b_prepared_absmax")
             return float(self.scalar.item())
 
     # ------------------------------------------------------------- winners --
