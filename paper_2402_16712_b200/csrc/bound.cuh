@@ -50,7 +50,7 @@ constexpr int kBMinBlocks = kBTgt == 64 ? 2 : 1;
 #define KB_STAGES 2
 #endif
 #ifndef KB_FLUSH
-#define KB_FLUSH (256 / KB_ROWS)  // chunks between FP32 -> FP64 residual flushes (<= 16 pair sums, see below)
+#define KB_FLUSH (128 / KB_ROWS)  // chunks between FP32 -> FP64 residual flushes (<= 16 rows, see below)
 #endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
 constexpr int kBRowsW = kBRows / kBRG;     // rows per warp per chunk
@@ -62,7 +62,7 @@ constexpr int kBHist = kBPiv * kNB * kBTgt * 4;  // [pivot][bin][target slot], e
 static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
 static_assert(kBTgt == 64 || kBTgt == 128, "k_tile lays out 64- or 128-target groups");
 static_assert(kBRowsW % 2 == 0 && kBRows % kBRG == 0, "a warp takes whole row pairs of a chunk");
-static_assert(KB_FLUSH * kBRowsW <= 32, "residual summation margin (column_bounds) covers 16 row pairs");
+static_assert(KB_FLUSH * kBRowsW <= 16, "residual summation margin (column_bounds) covers 16 rows per flush");
 static_assert(kBStages * kBStage >= kBRG * kBProb * 8, "stage buffers hold the warps' residual shares");
 constexpr int kBLamGroup = 4;              // penalties per pivot-sum round of a multi-penalty epilogue
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
@@ -135,8 +135,8 @@ struct ColumnBounds {
     // of its binned position, so f moves by at most pert when the rows are
     // moved into their bins; the bounds below hold for that moved problem
     pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
-    // (k_bound: each thread's FP32 accumulator takes <= 16 two-row sums between
-    // FP64 flushes, KB_FLUSH: relative error <= 17 u)
+    // (k_bound: each thread's FP32 accumulator adds <= 16 nonnegative row terms
+    // between FP64 flushes, KB_FLUSH: relative error <= 15 u / (1 - 15 u) < 20 u)
     eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
     // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
     // (slots 0..k).  The subgradient bounds at edge k are
@@ -621,13 +621,13 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   const unsigned hb = smem_u32(hist + th * kBTE * 32 + lane) - 0x4B000000u * (unsigned)(kBTgt * 4);
 
   unsigned fphase = 0;
-  float racc[kBPiv][kBTE];
+  float2 racc[kBPiv / 2][kBTE];  // (pivot 2h, pivot 2h + 1) pairs: one FADD2 per row
   double ec[kBPiv][kBTE];  // this warp's share of e_j(c) of the eight problems
 #pragma unroll
   for (int t = 0; t < kBPiv; ++t)
 #pragma unroll
     for (int ee = 0; ee < kBTE; ++ee) {
-      racc[t][ee] = 0.f;
+      if (t % 2 == 0) racc[t / 2][ee] = make_float2(0.f, 0.f);
       ec[t][ee] = 0.0;
     }
   int nflush = 0;
@@ -640,7 +640,6 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     const float4* rec = (const float4*)(sb + kBTile);       // [kBRows][3]
 #pragma unroll
     for (int u2 = 0; u2 < kBRowsW; u2 += 2) {
-      float rp[2][kBPiv][kBTE];  // x_ij - c x_ip of the row pair
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int r = rg * kBRowsW + u2 + v;
@@ -666,17 +665,11 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
             // fire-and-forget shared adds (the other warps add into the same bins)
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(w0));
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1), "r"(w1));
-            // x_ij - c x_ip (dropped rows: x_ij)
-            const float2 rr = ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee]));
-            rp[v][2 * h][ee] = rr.x;
-            rp[v][2 * h + 1][ee] = rr.y;
+            // |x_ij - c x_ip| of both pivots (dropped rows: |x_ij|)
+            racc[h][ee] = fadd2_abs(racc[h][ee], ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee])));
           }
         }
       }
-#pragma unroll
-      for (int t = 0; t < kBPiv; ++t)
-#pragma unroll
-        for (int ee = 0; ee < kBTE; ++ee) racc[t][ee] += fabsf(rp[0][t][ee]) + fabsf(rp[1][t][ee]);
     }
     if (++nflush == KB_FLUSH || c + 1 == nch) {
       nflush = 0;
@@ -684,8 +677,8 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
       for (int t = 0; t < kBPiv; ++t)
 #pragma unroll
         for (int ee = 0; ee < kBTE; ++ee) {
-          ec[t][ee] += (double)racc[t][ee];
-          racc[t][ee] = 0.f;
+          ec[t][ee] += (double)(t % 2 ? racc[t / 2][ee].y : racc[t / 2][ee].x);
+          if (t % 2) racc[t / 2][ee] = make_float2(0.f, 0.f);
         }
     }
     __syncwarp();
