@@ -174,6 +174,13 @@ int l1b_deflate(double* d_X, int64_t n, int64_t m, const double* d_v, double* d_
 /* max_ij |x_ij| into d_out[0] (the early-stop test of subspace.py:67,71). */
 int l1b_absmax(const double* d_X, int64_t n, int64_t m, double* d_out, void* stream);
 
+/* Host memcpy for the staging of an upload (no reference counterpart: the
+ * reference never leaves the host): dst <- src, `bytes` bytes, split over
+ * `threads` threads of a persistent pool (<= 0: 8), written with streaming
+ * stores so the pinned destination is not left dirty in the CPU caches when
+ * the copy engine reads it (hostcopy.inc). */
+int l1b_host_copy(void* dst, const void* src, size_t bytes, int32_t threads);
+
 /* The same max_ij |x_ij| of the matrix the workspace was last prepared for
  * (l1b_prepare computes it with the column statistics): one 8-byte copy into
  * d_out[0] on the stream, no pass over X. */

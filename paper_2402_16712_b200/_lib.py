@@ -29,6 +29,7 @@ ABI_SYMBOLS = (
     "l1b_deflate",
     "l1b_absmax",
     "l1b_prepared_absmax",
+    "l1b_host_copy",
     "l1b_selftest_divide",
     "l1b_kernel_launches",
     "l1b_dfma_probe",
@@ -118,6 +119,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_deflate.argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
     lib.l1b_absmax.restype = ctypes.c_int
     lib.l1b_absmax.argtypes = [_vp, _i64, _i64, _vp, _vp]
+    lib.l1b_host_copy.restype = ctypes.c_int
+    lib.l1b_host_copy.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int32]
     lib.l1b_prepared_absmax.restype = ctypes.c_int
     lib.l1b_prepared_absmax.argtypes = [_vp, _i64, _i64, ctypes.c_size_t, _vp, _vp]
     lib.l1b_selftest_divide.restype = ctypes.c_int

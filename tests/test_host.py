@@ -139,6 +139,22 @@ def test_abi_library_exports_every_header_symbol():
     assert lib.l1b_status_string(-1) == b"invalid argument"
 
 
+def test_host_copy_is_memcpy():
+    """l1b_host_copy (the upload's staging copy, hostcopy.inc): the same bytes as
+    memcpy for any alignment and size, through the thread pool and without it."""
+    lib = _lib.load()
+    rng = np.random.default_rng(5)
+    src = rng.integers(0, 256, (5 << 20) + 77, dtype=np.uint8)
+    for size, so, do, threads in [(0, 0, 0, 8), (1, 3, 5, 8), (31, 1, 0, 1), (4096, 0, 7, 8),
+                                  ((1 << 20) + 7, 5, 3, 8), ((5 << 20) + 60, 17, 11, 8), ((3 << 20) + 1, 0, 0, 3),
+                                  ((2 << 20) + 9, 2, 1, 64)]:
+        dst = np.zeros(size + do + 64, dtype=np.uint8)
+        assert lib.l1b_host_copy(dst.ctypes.data + do, src.ctypes.data + so, size, threads) == _lib.L1B_OK
+        assert np.array_equal(dst[do:do + size], src[so:so + size]), (size, so, do, threads)
+        assert not dst[:do].any() and not dst[do + size:].any()
+    assert lib.l1b_host_copy(None, None, 8, 4) == _lib.L1B_EINVAL
+
+
 def test_abi_workspace_and_argument_checks():
     lib = _lib.load()
     assert lib.l1b_workspace_bytes(2000, 2000, 1, 2000) > 2000 * 2000 * 32
