@@ -516,15 +516,17 @@ def run_ours(args):
         sel_ms.append(ms)
     sel_ms = float(np.median(sel_ms))
     strag = eng.straggler_counts(npiv)[0]
-    # the pruned step's dominant kernel: k_bound<1>, the bounding pass over
-    # every problem, timed by the library's CUDA events on its stream
+    # the pruned step's dominant kernel: k_bound, the bounding pass over every
+    # problem exactly as the step runs it (fit_line's lean first pass; a
+    # sweep's multi-penalty pass), timed by the library's CUDA events on its
+    # stream
     bnd_ms, kb_ms = [], []
     ulams = sorted(set(float(x) for x in lams))
     multi = len(ulams) > 1 and all(np.isfinite(ulams))  # a sweep bounds every penalty in one pass
     for _ in range(max(3, min(args.steps, 5))):
         flush.fill_(1)
         ms, _ = _sync_time(stream, (lambda: eng.bound_pivots_multi(ulams, p_begin, p_stride, npiv)) if multi
-                           else (lambda: eng.bound_pivots(lams[0], p_begin, p_stride, npiv)))
+                           else (lambda: eng.bound_pivot_sums(lams[0], p_begin, p_stride, npiv)))
         bnd_ms.append(ms)
         kb = ctypes.c_float()
         _lib.check(lib.l1b_last_bound_ms(ctypes.byref(kb)), "l1b_last_bound_ms")

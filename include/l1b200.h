@@ -85,6 +85,16 @@ int l1b_fit_pivot_list(const double* d_X, int64_t n, int64_t m, const double* h_
 int l1b_bound_pivots(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
                      int64_t npiv, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes, void* stream);
 
+/* The same per-pivot bounds from fit_line's own first pass (the pass
+ * l1b_fit_line runs before its cascade): per-pivot sums only -- no per-column
+ * bounds or seeds are left in the workspace, so the pass writes 8 bytes per
+ * problem (its next range) instead of 48.  steer = 0: one pass over every
+ * row; steer = s > 1: a pass over every s-th 64-row chunk first narrows the
+ * brackets (tall data, l1b_set_steer). */
+int l1b_bound_pivot_sums(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_begin, int64_t p_stride,
+                         int64_t npiv, int32_t steer, double* d_lb, double* d_ub, void* d_ws, size_t ws_bytes,
+                         void* stream);
+
 /* Algorithm 2 (path.py:76-102) for one pivot: for every target column
  * c (targets j != pivot in ascending order) the tableau's column in stable
  * (ratio, row) order (ratios.py:109-135): d_ratios[c*ld + k] = r_k,

@@ -23,6 +23,7 @@ ABI_SYMBOLS = (
     "l1b_fit_pivots",
     "l1b_fit_pivot_list",
     "l1b_bound_pivots",
+    "l1b_bound_pivot_sums",
     "l1b_bound_pivot_list",
     "l1b_argmin",
     "l1b_residual_exact",
@@ -108,6 +109,9 @@ def load() -> ctypes.CDLL:
                                        ctypes.POINTER(ctypes.c_int64), _i64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_bound_pivots.restype = ctypes.c_int
     lib.l1b_bound_pivots.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_bound_pivot_sums.restype = ctypes.c_int
+    lib.l1b_bound_pivot_sums.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, _i32, _vp, _vp, _vp,
+                                         _sz, _vp]
     lib.l1b_bound_pivot_list.restype = ctypes.c_int
     lib.l1b_bound_pivot_list.argtypes = [_vp, _i64, _i64, ctypes.c_double, ctypes.POINTER(ctypes.c_int64), _i64,
                                          _i32, _vp, _vp, _vp, _sz, _vp]

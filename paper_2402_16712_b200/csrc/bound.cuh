@@ -537,12 +537,25 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int th = warp % kBTH, rg = warp / kBTH;
   const int64_t n = P.n, m = P.m, np = P.np;
-  const int64_t tile0 = (int64_t)blockIdx.x * kBE;            // this CTA's first 32-target tile of Xft
-  const int64_t gbase = (int64_t)blockIdx.y * np;              // this CTA's pivot group in the plane (rows)
+  // CTA -> (target group bx, pivot group by).  Plain order is target-group
+  // fastest; when the target tiles outgrow L2 (tall and wide data) the groups
+  // are cut into bands of P.band target groups, pivot-group-major inside a
+  // band, so the CTAs resident together share one band's tiles in L2 instead
+  // of each pulling a different tile from HBM
+  int64_t bx, by;
+  {
+    const int64_t T = gridDim.x, G = gridDim.y, L = (int64_t)blockIdx.y * T + blockIdx.x;
+    const int64_t B = min((int64_t)P.band, T), band = L / (B * G), rem = L - band * B * G;
+    const int64_t bw = min(B, T - band * B);
+    by = rem / bw;
+    bx = band * B + rem % bw;
+  }
+  const int64_t tile0 = bx * kBE;    // this CTA's first 32-target tile of Xft
+  const int64_t gbase = by * np;     // this CTA's pivot group in the plane (rows)
 
   // the metadata of this thread's epilogue problem q = tid
   const int qt = tid / kBTgt, qs = tid % kBTgt;  // pivot, target slot (e * 32 + lane)
-  const int64_t qk = (int64_t)blockIdx.y * kBPiv + qt;
+  const int64_t qk = by * kBPiv + qt;
   const int64_t qj = tile0 * 32 + qs;
   auto meta = [&](int64_t& pv, bool& okk, bool& dg, double& T, double& u) {
     okk = qk < P.npiv;
@@ -564,7 +577,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     const int64_t i0 = (cb + c * cstep) * kBRows;
     unsigned char* base = smem + (size_t)st * kBStage;
     mbar_expect_tx(&full[st], (unsigned)(kBTile + kBPlane));
-    bulk_g2s(base, P.Xq + ((int64_t)blockIdx.x * np + i0) * kBTgt, kBTile, &full[st]);
+    bulk_g2s(base, P.Xq + (bx * np + i0) * kBTgt, kBTile, &full[st]);
     bulk_g2s(base + kBTile, P.gbp + (gbase + i0) * 3, kBPlane, &full[st]);
   };
   if (tid == 0) {
@@ -741,7 +754,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     __syncthreads();
     constexpr int WP = kBWarps / kBPiv;  // warps per pivot (q = tid: pivot t = warp / WP)
     if (P.LBq && tid < kBPiv) {
-      const int64_t k = (int64_t)blockIdx.y * kBPiv + tid;
+      const int64_t k = by * kBPiv + tid;
       if (k < P.npiv) {
         unsigned long long sl = 0, su = 0;
         for (int w = tid * WP; w < (tid + 1) * WP; ++w) {
@@ -789,7 +802,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     constexpr int WP = kBWarps / kBPiv;
     if (tid < kBPiv * kBLamGroup) {
       const int t = tid / kBLamGroup, g = tid % kBLamGroup;
-      const int64_t k = (int64_t)blockIdx.y * kBPiv + t;
+      const int64_t k = by * kBPiv + t;
       if (k < P.npiv && l0 + g < P.nlam) {
         unsigned long long sl = 0, su = 0;
         for (int w = t * WP; w < (t + 1) * WP; ++w) {

@@ -97,6 +97,7 @@ struct SelParams {
   const int* fxk;        // fixed-point exponent (k_fxscale)
   int lean;              // k_bound: per-pivot sums and next ranges only (no LB / UB / BRK records)
   int steer;             // k_bound: a steering pass over every steer-th row chunk (next ranges only)
+  int band;              // k_bound: target groups per raster band (>= gridDim.x: plain order)
 };
 
 __device__ __forceinline__ int64_t pivot_of(const SelParams& P, int64_t kk) {

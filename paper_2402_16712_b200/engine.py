@@ -247,6 +247,21 @@ class DeviceFit:
         _lib.check(rc, "l1b_fit_pivot_list_seeded")
         return V, err, pen, obj
 
+    def bound_pivot_sums(self, lam: float, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None,
+                         steer: int = 0):
+        """The same bounds from fit_line's lean first pass (l1b_bound_pivot_sums): per-pivot
+        sums only, no per-column bounds left behind."""
+        if npiv is None:
+            npiv = shard(self.m - p_begin, 0, p_stride)[2] if p_stride > 1 else self.m - p_begin
+        with torch.cuda.device(self.device):
+            b = torch.empty((2, npiv), dtype=torch.float64, device=self.device)
+            rc = self.lib.l1b_bound_pivot_sums(self.X.data_ptr(), self.n, self.m, float(lam), p_begin, p_stride,
+                                               npiv, int(steer), b[0].data_ptr(), b[1].data_ptr(), self.ws.data_ptr(),
+                                               self.ws.numel(), self._s)
+            _lib.check(rc, "l1b_bound_pivot_sums")
+            bh = b.cpu().numpy()
+        return bh[0], bh[1]
+
     def bound_pivots(self, lam: float, p_begin: int = 0, p_stride: int = 1, npiv: int | None = None):
         """Rigorous bounds lb <= z_p <= ub of every shard pivot's objective (host arrays)."""
         if npiv is None:

@@ -339,10 +339,15 @@ def test_use_gpu_patches_reference_bindings():
 
 def _bounds_hold(X, lam):
     eng = DeviceFit(X)
-    lb, ub = eng.bound_pivots(lam)
     _, _, _, O = eng.fit_pivots([lam], want_v=False)
     o = O.cpu().numpy()[0]
     tol = 1e-12 * np.abs(o) + OBJ_ATOL * float(np.abs(X).sum())
+    # fit_line's lean first pass (per-pivot sums only), unsteered and steered
+    for steer in (0, 2):
+        lb, ub = eng.bound_pivot_sums(lam, steer=steer)
+        assert np.all(lb <= o + tol), (lam, steer, np.max(lb - o))
+        assert np.all(o <= ub + tol), (lam, steer, np.max(o - ub))
+    lb, ub = eng.bound_pivots(lam)
     assert np.all(lb <= o + tol), (lam, np.max(lb - o))
     assert np.all(o <= ub + tol), (lam, np.max(o - ub))
     # per column: lb_pj <= f_pj* <= ub_pj with f_pj* from the exact directions
