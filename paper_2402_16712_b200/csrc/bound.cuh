@@ -50,7 +50,7 @@ constexpr int kBMinBlocks = kBTgt == 64 ? 2 : 1;
 #define KB_STAGES 2
 #endif
 #ifndef KB_FLUSH
-#define KB_FLUSH (128 / KB_ROWS)  // chunks between FP32 -> FP64 residual flushes (<= 16 rows, see below)
+#define KB_FLUSH (256 / KB_ROWS)  // chunks between FP32 -> FP64 residual flushes (<= 16 row pairs, see below)
 #endif
 constexpr int kBRows = KB_ROWS;            // rows per staged chunk
 constexpr int kBRowsW = kBRows / kBRG;     // rows per warp per chunk
@@ -62,7 +62,7 @@ constexpr int kBHist = kBPiv * kNB * kBTgt * 4;  // [pivot][bin][target slot], e
 static_assert(kBPiv == kGroupBoundPiv, "k_bound reads k_group_bound's plane groups");
 static_assert(kBTgt == 64 || kBTgt == 128, "k_tile lays out 64- or 128-target groups");
 static_assert(kBRowsW % 2 == 0 && kBRows % kBRG == 0, "a warp takes whole row pairs of a chunk");
-static_assert(KB_FLUSH * kBRowsW <= 16, "residual summation margin (column_bounds) covers 16 rows per flush");
+static_assert(KB_FLUSH * kBRowsW <= 32, "residual summation margin (column_bounds) covers 16 row pairs per flush");
 static_assert(kBStages * kBStage >= kBRG * kBProb * 8, "stage buffers hold the warps' residual shares");
 constexpr int kBLamGroup = 4;              // penalties per pivot-sum round of a multi-penalty epilogue
 constexpr size_t kBoundSmem = (size_t)kBStages * kBStage + kBHist;
@@ -135,8 +135,8 @@ struct ColumnBounds {
     // of its binned position, so f moves by at most pert when the rows are
     // moved into their bins; the bounds below hold for that moved problem
     pert = 0x1p-22 * colsum + T * (0x1p-21 * (fabs(lo) + fabs(hi)) + 0x1p-20 * w);
-    // (k_bound: each thread's FP32 accumulator adds <= 16 nonnegative row terms
-    // between FP64 flushes, KB_FLUSH: relative error <= 15 u / (1 - 15 u) < 20 u)
+    // (k_bound: each thread's FP32 accumulator adds <= 16 two-row sums of
+    // nonnegative terms between FP64 flushes, KB_FLUSH: relative error <= 17 u)
     eps = 0x1p-22 * (colsum + fabs(c) * T) + 20.0 * 0x1p-24 * ec + pert;
     // edges e_k = lo + k w (k = 0..62); C_k = q Cu_k = weight with r < e_k
     // (slots 0..k).  The subgradient bounds at edge k are
@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     const float4* rec = (const float4*)(sb + kBTile);       // [kBRows][3]
 #pragma unroll
     for (int u2 = 0; u2 < kBRowsW; u2 += 2) {
+      float2 rr[2][kBPiv / 2][kBTE];  // x_ij - c x_ip of the row pair, pivots (2h, 2h + 1)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int r = rg * kBRowsW + u2 + v;
@@ -678,11 +679,18 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
             // fire-and-forget shared adds (the other warps add into the same bins)
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(w0));
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1), "r"(w1));
-            // |x_ij - c x_ip| of both pivots (dropped rows: |x_ij|)
-            racc[h][ee] = fadd2_abs(racc[h][ee], ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee])));
+            // x_ij - c x_ip of both pivots (dropped rows: x_ij)
+            rr[v][h][ee] = ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee]));
           }
         }
       }
+      // the row pair's |terms| summed first, then added (two FADD2 per four
+      // elements; the pair sums keep the accumulation error at 16 u per flush)
+#pragma unroll
+      for (int h = 0; h < kBPiv / 2; ++h)
+#pragma unroll
+        for (int ee = 0; ee < kBTE; ++ee)
+          racc[h][ee] = fadd2(racc[h][ee], fadd2(fabs2(rr[0][h][ee]), fabs2(rr[1][h][ee])));
     }
     if (++nflush == KB_FLUSH || c + 1 == nch) {
       nflush = 0;
