@@ -415,6 +415,30 @@ def test_pruned_fit_equals_full_fit():
             assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
 
 
+def test_raster_bands_leave_bounds_unchanged(monkeypatch):
+    """k_bound's raster bands (CTAs pivot-group-major inside bands of target
+    groups, used when the target tiles outgrow L2) only reorder the CTAs: the
+    per-pivot bounds are integer sums, so every band width -- a ragged last band
+    included -- gives the same bits, single- and multi-penalty, and the pruned
+    fit is still the full fit."""
+    d, _ = l1b.gen_line_data(330, 1500, seed=8, noise_scale=1.0)  # 6 target groups of 64
+    X = d.values
+    eng = DeviceFit(X)
+    lams = [0.0, 1.0, 300.0]
+    monkeypatch.delenv("L1B200_BAND", raising=False)
+    ref = eng.bound_pivot_sums(1.0)
+    refm = eng.bound_pivots_multi(lams)
+    full = eng.shard_winners([1.0], prune=False)[0]
+    for band in ("1", "4", "5"):
+        monkeypatch.setenv("L1B200_BAND", band)
+        got = eng.bound_pivot_sums(1.0)
+        assert got[0].tobytes() == ref[0].tobytes() and got[1].tobytes() == ref[1].tobytes(), band
+        gotm = eng.bound_pivots_multi(lams)
+        assert all(np.array_equal(a, b) for a, b in zip(gotm[:2], refm[:2])), band
+        w = eng.shard_winners([1.0], prune=True)[0]
+        assert w.pivot == full.pivot and w.v.tobytes() == full.v.tobytes() and w.objective == full.objective
+
+
 def test_pruned_fit_equals_full_fit_tall():
     """Tall columns (n >= 2 * KB_SREP_ROWS = 8192) start the bound pass from several
     averaged row samples (k_bound<..., TALL>); single- and multi-penalty pruned

@@ -30,6 +30,7 @@ for rep in range(a.reps):
     for t in range(a.k):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        eng.set_steer(0 if t == 0 else -1)  # fit_subspace's policy (api.fit_subspace, bench.py)
         w = eng.shard_winners([a.lam])[0]
         torch.cuda.synchronize()
         t1 = time.perf_counter()
