@@ -192,7 +192,7 @@ class DeviceFit:
     def deflate(self, v) -> None:
         """subspace.py:22-36 in place on the device copy, then re-prepare."""
         with torch.cuda.device(self.device):
-            v_dev = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).to(self.device)
+            v_dev = torch.tensor(np.asarray(v, dtype=np.float64), device=self.device)  # a copy: v may be read-only
             _lib.check(self.lib.l1b_deflate(self.X.data_ptr(), self.n, self.m, v_dev.data_ptr(),
                                             self.tmp.data_ptr(), self._s), "l1b_deflate")
         self.prepare()
