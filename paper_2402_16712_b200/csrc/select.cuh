@@ -81,6 +81,7 @@ struct SelParams {
   double2* BRK;          // bound mode: [npiv][m] range holding each column's optimum v
   const int64_t* seeds;  // seeded fit / continued bound: position in the previous bound call's list
   const float2* NEXTr;   // bound mode: ranges the previous pass left ([npiv][m])
+  const float2* win;     // k_select: per-problem windows from k_bound passes (no sample / F passes)
   float2* NEXTw;         // bound mode: ranges this pass leaves
   int delta;             // bound mode: sample bracket half-width (ranks)
   unsigned* GH;          // split bound: merged histograms [npiv*m][64]
@@ -197,7 +198,11 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
     Lsc = ldexp(P.lam, sp);
   }
   const double unit = ldexp(1.0, -sp);
-  const bool exact_f = P.nfloat >= 2;  // multi-pass: exact bases and exact Wneg in the F passes
+  // windows handed in by k_bound passes (fit_impl's seeded windows): no sample
+  // bracket and no F passes, pass B starts on them (a missed crossing or an
+  // overflowing window goes to the straggler solver, as always)
+  const bool winm = P.win != nullptr;
+  const bool exact_f = !winm && P.nfloat >= 2;  // multi-pass: exact bases and exact Wneg in the F passes
 
   // ---- TMA pipeline ----------------------------------------------------------
   // Producer: the lanes of warp 0 issue the bulk copies of chunk c into stage
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   stamp(0);
   // ---- sample: float ratios of 32 strided rows, sorted -> value bracket ----
   float lo = 0.f, hi = 0.f;
-  if (active) {
+  if (active && !winm) {
     float sr[kSample], sw[kSample];
 #pragma unroll
     for (int s = 0; s < kSample; ++s) {
@@ -343,7 +348,12 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   bool live = active;
   double Lw = -kBig, Hw = kBig;   // final window [Lw, Hw)
   float G32 = 0.f;
-  for (int pass = 0; pass < P.nfloat; ++pass) {
+  if (winm && active) {
+    const float2 r = P.win[kk * m + j];
+    Lw = (double)r.x;
+    Hw = (double)r.y;
+  }
+  for (int pass = 0; pass < (winm ? 0 : P.nfloat); ++pass) {
     const float A = (62.f / 63.f) / (hi - lo);
     const float B = 0.5f / 63.f - lo * A;
 #pragma unroll
