@@ -250,6 +250,25 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
                  double* d_v, double* h_err, double* h_pen, double* h_obj, int64_t* h_candidates, void* d_ws,
                  size_t ws_bytes, void* stream);
 
+/* Vector form of the exchange hook (a penalty sweep): replaces tops[0..count)
+ * -- this shard's best upper bound per penalty -- by the best over all shards. */
+typedef void (*l1b_ub_exchange_vec_fn)(double* tops, int32_t count, void* ctx);
+
+/* fit_lines for one pivot shard in one call: every penalty of h_lams (>= 2
+ * distinct finite values; any order, repeats allowed) bounded by one
+ * multi-penalty pass, the survivors of all penalties refined and fitted as one
+ * entry list per level, the near-minimal candidates re-scored in NumPy's order.
+ * Per input penalty j: h_pivot[j] (-1 when another shard provably wins),
+ * d_v[j*m .. j*m+m), h_err[j], h_pen[j], h_obj[j].  d_bounds: device scratch of
+ * 2 * L * npiv doubles (L distinct penalties); d_ranges (may be NULL): device
+ * scratch of ranges_bytes >= 8 L npiv m for the per-penalty next ranges (the
+ * first refinement level continues from them).  Synchronises the stream. */
+int l1b_fit_lines(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam, int64_t p_begin,
+                  int64_t p_stride, int64_t npiv, l1b_ub_exchange_vec_fn ub_exchange, void* exchange_ctx,
+                  double* d_bounds, void* d_ranges, size_t ranges_bytes, int64_t* h_pivot, double* d_v,
+                  double* h_err, double* h_pen, double* h_obj, int64_t* h_candidates, void* d_ws, size_t ws_bytes,
+                  void* stream);
+
 /* Entry lists (a penalty sweep's survivors, batched): count (pivot, penalty)
  * entries h_pivots[k], h_lams[k] in one launch.  l1b_bound_entries is one
  * bounding pass per entry -- from row samples at the entry's penalty, or,

@@ -48,6 +48,7 @@ ABI_SYMBOLS = (
     "l1b_fit_entries_seeded",
     "l1b_residual_exact_batch",
     "l1b_fit_line",
+    "l1b_fit_lines",
     "l1b_csv_read",
     "l1b_csv_free",
     "l1b_merge_path",
@@ -61,6 +62,7 @@ ABI_SYMBOLS = (
 
 # double (*)(double top, void* ctx): the sharded fit's upper-bound exchange hook
 UB_EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_double, ctypes.c_void_p)
+UB_EXCHANGE_VEC_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_void_p)
 
 L1B_OK = 0
 L1B_EINVAL = -1
@@ -166,6 +168,9 @@ def load() -> ctypes.CDLL:
     lib.l1b_fit_line.restype = ctypes.c_int
     lib.l1b_fit_line.argtypes = [_vp, _i64, _i64, ctypes.c_double, _i64, _i64, _i64, ctypes.c_int32, UB_EXCHANGE_FN,
                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    lib.l1b_fit_lines.restype = ctypes.c_int
+    lib.l1b_fit_lines.argtypes = [_vp, _i64, _i64, _vp, _i32, _i64, _i64, _i64, UB_EXCHANGE_VEC_FN, _vp, _vp, _vp, _sz,
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     lib.l1b_csv_read.restype = ctypes.c_int
     lib.l1b_csv_read.argtypes = [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32,
                                  ctypes.POINTER(ctypes.POINTER(ctypes.c_double)), ctypes.POINTER(ctypes.c_int64),

@@ -211,4 +211,219 @@ int l1b_fit_line(const double* d_X, int64_t n, int64_t m, double lam, int64_t p_
   return L1B_OK;
 }
 
+
+// A penalty sweep (fit_lines) for one pivot shard in one call: the cascade of
+// engine.DeviceFit._sweep_winners in C++ (one multi-penalty bound pass, every
+// penalty's survivors refined and fitted as one entry list per level, the
+// near-minimal candidates re-scored in NumPy's order), so a step makes no
+// Python round trips between its synchronisations.
+int l1b_fit_lines(const double* d_X, int64_t n, int64_t m, const double* h_lams, int32_t nlam, int64_t p_begin,
+                  int64_t p_stride, int64_t npiv, l1b_ub_exchange_vec_fn ub_exchange, void* exchange_ctx,
+                  double* d_bounds, void* d_ranges, size_t ranges_bytes, int64_t* h_pivot, double* d_v,
+                  double* h_err, double* h_pen, double* h_obj, int64_t* h_candidates, void* d_ws, size_t ws_bytes,
+                  void* stream) {
+  if (!d_X || !h_lams || !d_bounds || !h_pivot || !d_v || !h_err || !h_pen || !h_obj || n < 1 || m < 2 ||
+      nlam < 1 || npiv < 1)
+    return L1B_EINVAL;
+  if (p_stride < 1 || p_begin < 0 || p_begin + (npiv - 1) * p_stride >= m) return L1B_EINVAL;
+  std::vector<double> uniq(h_lams, h_lams + nlam);
+  for (double x : uniq)
+    if (!(x >= 0.0) || !std::isfinite(x)) return L1B_EINVAL;
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  const int32_t L = (int32_t)uniq.size();
+  if (L < 2) return L1B_EINVAL;  // one penalty: l1b_fit_line
+  Workspace w;
+  const int64_t cap = ws_capacity(n, m, ws_bytes);
+  if (cap < npiv) return L1B_ENOMEM;
+  carve(&w, d_ws, n, m, cap);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto sync = [&]() { return cudaStreamSynchronize(s) == cudaSuccess; };
+  double* d_lb = w.drv;
+  double* d_ub = w.drv + cap;
+  double* d_err = w.drv + 2 * cap;
+  double* d_pen = w.drv + 3 * cap;
+  double* d_obj = w.drv + 4 * cap;
+  // one bounding pass for every penalty; its per-penalty next ranges let the
+  // first refinement level continue instead of re-sampling
+  const bool keep = d_ranges && ranges_bytes >= (size_t)L * (size_t)npiv * (size_t)m * sizeof(float2);
+  int st = l1b_bound_pivots_multi(d_X, n, m, uniq.data(), L, p_begin, p_stride, npiv, d_bounds,
+                                  d_bounds + (size_t)L * npiv, keep ? d_ranges : nullptr, d_ws, ws_bytes, stream);
+  if (st != L1B_OK) return st;
+  std::vector<double> lbm((size_t)L * npiv), ubm((size_t)L * npiv);
+  double amax = 0.0;
+  if (cudaMemcpyAsync(&amax, w.flags + 6, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(lbm.data(), d_bounds, sizeof(double) * lbm.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(ubm.data(), d_bounds + (size_t)L * npiv, sizeof(double) * ubm.size(), cudaMemcpyDeviceToHost,
+                      s) != cudaSuccess || !sync())
+    return L1B_ECUDA;
+  const double abs_scale = amax * (double)n * (double)m;
+  auto thr = [&](double top) {
+    return std::isfinite(top) ? top + kPruneRtol * fabs(top) + kRescoreAtol * abs_scale : INFINITY;
+  };
+  std::vector<double> tops(L, INFINITY);
+  for (int32_t i = 0; i < L; ++i)
+    for (int64_t k = 0; k < npiv; ++k) tops[i] = std::min(tops[i], ubm[(size_t)i * npiv + k]);
+  if (ub_exchange) ub_exchange(tops.data(), L, exchange_ctx);  // every penalty's best over all shards
+  std::vector<std::vector<int64_t>> ent(L);
+  for (int32_t i = 0; i < L; ++i)
+    for (int64_t k = 0; k < npiv; ++k)
+      if (!(lbm[(size_t)i * npiv + k] > thr(tops[i]))) ent[i].push_back(k);  // NaN-safe: keep unless worse
+  // entry lists are bounded by the workspace's pivot capacity
+  std::vector<std::vector<int32_t>> batches;
+  {
+    std::vector<int32_t> cur;
+    int64_t size = 0;
+    for (int32_t i = 0; i < L; ++i) {
+      const int64_t c = (int64_t)ent[i].size();
+      if (!cur.empty() && size + c > cap) {
+        batches.push_back(cur);
+        cur.clear();
+        size = 0;
+      }
+      cur.push_back(i);
+      size += c;
+    }
+    if (!cur.empty()) batches.push_back(cur);
+  }
+  std::vector<int64_t> wpiv(L, -1);
+  std::vector<double> werr(L, 0.0), wpen(L, 0.0), wobj(L, 0.0);
+  std::vector<std::vector<double>> wv(L);
+  int64_t ncand = 0;
+  for (const auto& bl : batches) {
+    std::vector<int32_t> li;
+    std::vector<int64_t> kk, seed;
+    for (int32_t i : bl)
+      for (int64_t k : ent[i]) {
+        li.push_back(i);
+        kk.push_back(k);
+      }
+    int64_t seed_n = 0;
+    const void* src = nullptr;
+    if (keep) {  // level 0 continues from the multi pass's per-penalty ranges
+      seed.resize(li.size());
+      for (size_t e = 0; e < li.size(); ++e) seed[e] = (int64_t)li[e] * npiv + kk[e];
+      seed_n = (int64_t)L * npiv;
+      src = d_ranges;
+    }
+    std::vector<double> lam_e, lb2, ub2;
+    std::vector<int64_t> piv_e;
+    auto entries = [&]() {
+      lam_e.resize(li.size());
+      piv_e.resize(li.size());
+      for (size_t e = 0; e < li.size(); ++e) {
+        lam_e[e] = uniq[li[e]];
+        piv_e[e] = p_begin + kk[e] * p_stride;
+      }
+    };
+    for (int level = 0; level <= kRefinePasses; ++level) {
+      if (kk.empty()) break;
+      if (level > 0) {
+        std::vector<int64_t> counts(L, 0);
+        for (int32_t i : li) ++counts[i];
+        if (std::all_of(counts.begin(), counts.end(), [](int64_t c) { return c <= kRefineMin; })) break;
+      }
+      entries();
+      const int64_t K = (int64_t)li.size();
+      st = l1b_bound_entries(d_X, n, m, lam_e.data(), piv_e.data(), K, seed.empty() ? nullptr : seed.data(),
+                             seed_n, src, d_lb, d_ub, d_ws, ws_bytes, stream);
+      if (st != L1B_OK) return st;
+      src = nullptr;
+      lb2.resize(K);
+      ub2.resize(K);
+      if (cudaMemcpyAsync(lb2.data(), d_lb, sizeof(double) * K, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaMemcpyAsync(ub2.data(), d_ub, sizeof(double) * K, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          !sync())
+        return L1B_ECUDA;
+      for (int64_t e = 0; e < K; ++e) tops[li[e]] = std::min(tops[li[e]], ub2[e]);
+      std::vector<int32_t> nli;
+      std::vector<int64_t> nkk, sel;
+      for (int64_t e = 0; e < K; ++e)
+        if (!(lb2[e] > thr(tops[li[e]]))) {
+          nli.push_back(li[e]);
+          nkk.push_back(kk[e]);
+          sel.push_back(e);
+        }
+      li.swap(nli);
+      kk.swap(nkk);
+      seed.swap(sel);
+      seed_n = K;
+    }
+    ncand += (int64_t)kk.size();
+    if (kk.empty()) continue;
+    entries();
+    const int64_t K = (int64_t)li.size();
+    st = l1b_fit_entries_seeded(d_X, n, m, lam_e.data(), piv_e.data(), K, seed.data(), seed_n, nullptr, d_err, d_pen,
+                                d_obj, d_ws, ws_bytes, stream);
+    if (st != L1B_OK) return st;
+    std::vector<double> obj(K);
+    if (cudaMemcpyAsync(obj.data(), d_obj, sizeof(double) * K, cudaMemcpyDeviceToHost, s) != cudaSuccess || !sync())
+      return L1B_ECUDA;
+    // near-minimal candidates of every penalty (engine._candidates), ascending pivot order
+    std::vector<int64_t> ce_idx;  // entry index of each candidate
+    std::vector<int32_t> ce_lam;  // its penalty
+    for (int32_t i : bl) {
+      double best = INFINITY;
+      bool any = false;
+      for (int64_t e = 0; e < K; ++e)
+        if (li[e] == i) {
+          if (std::isnan(obj[e])) return L1B_EINVAL;
+          best = std::min(best, obj[e]);
+          any = true;
+        }
+      if (!any) continue;
+      for (int64_t e = 0; e < K; ++e) {
+        if (li[e] != i) continue;
+        const bool near = std::isinf(best) ? obj[e] == best
+                                           : obj[e] <= best + kRescoreRtol * fabs(best) + kRescoreAtol * abs_scale +
+                                                           1e-300;
+        if (near) {
+          ce_idx.push_back(e);
+          ce_lam.push_back(i);
+          if (std::isinf(best)) break;
+        }
+      }
+    }
+    const int64_t C = (int64_t)ce_idx.size();
+    for (int64_t c = 0; c < C; ++c)
+      if (cudaMemcpyAsync(w.ework + c * m, w.vwork + ce_idx[c] * m, sizeof(double) * m, cudaMemcpyDeviceToDevice,
+                          s) != cudaSuccess)
+        return L1B_ECUDA;
+    std::vector<int64_t> cp(C);
+    for (int64_t c = 0; c < C; ++c) cp[c] = piv_e[ce_idx[c]];
+    st = l1b_residual_exact_batch(d_X, n, m, w.ework, m, cp.data(), C, d_err, d_ws, ws_bytes, stream);
+    if (st != L1B_OK) return st;
+    std::vector<double> errs(C), vh((size_t)C * m), av(m);
+    if (cudaMemcpyAsync(errs.data(), d_err, sizeof(double) * C, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(vh.data(), w.ework, sizeof(double) * C * m, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        !sync())
+      return L1B_ECUDA;
+    for (int64_t c = 0; c < C; ++c) {  // first strict minimum per penalty, in pivot order (fit.py:98-102)
+      const int32_t i = ce_lam[c];
+      for (int64_t j = 0; j < m; ++j) av[j] = fabs(vh[(size_t)c * m + j]);
+      const double pn = np_pairwise(av.data(), m);
+      const double z = errs[c] + uniq[i] * pn;
+      if (wpiv[i] < 0 || z < wobj[i]) {
+        wpiv[i] = cp[c];
+        werr[i] = errs[c];
+        wpen[i] = pn;
+        wobj[i] = z;
+        wv[i].assign(vh.begin() + (size_t)c * m, vh.begin() + (size_t)(c + 1) * m);
+      }
+    }
+  }
+  if (h_candidates) *h_candidates = ncand;
+  for (int32_t j = 0; j < nlam; ++j) {
+    const int32_t i = (int32_t)(std::lower_bound(uniq.begin(), uniq.end(), h_lams[j]) - uniq.begin());
+    h_pivot[j] = wpiv[i];
+    h_err[j] = werr[i];
+    h_pen[j] = wpen[i];
+    h_obj[j] = wobj[i];
+    if (wpiv[i] >= 0 &&
+        cudaMemcpyAsync(d_v + (size_t)j * m, wv[i].data(), sizeof(double) * m, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess)
+      return L1B_ECUDA;
+  }
+  return sync() ? L1B_OK : L1B_ECUDA;
+}
 }  // extern "C"

@@ -579,10 +579,11 @@ class DeviceFit:
             # the per-penalty next ranges (8 B per (penalty, pivot, target)) let the
             # first refinement level continue instead of re-sampling
             keep_ranges = uniq.size * npiv * self.m * 8 <= (4 << 30) and os.environ.get("L1B200_SWEEP_RANGES", "1") != "0"
-            res = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv, ranges=keep_ranges)
-            lbm, ubm = res[0], res[1]
-            rg = res[2] if keep_ranges else None
-            return self._sweep_winners(lam, all_piv, lbm, ubm, uniq, ub_exchange, rg, npiv)
+            if os.environ.get("L1B200_PY_SWEEP", "0") == "1":  # the same cascade driven from Python (cross-check)
+                res = self.bound_pivots_multi(uniq, p_begin, p_stride, npiv, ranges=keep_ranges)
+                rg = res[2] if keep_ranges else None
+                return self._sweep_winners(lam, all_piv, res[0], res[1], uniq, ub_exchange, rg, npiv)
+            return self.fit_lines_device(lam, p_begin, p_stride, npiv, ub_exchange, keep_ranges)
         for l in range(lam.size):
             lb, ub = self.bound_pivots(float(lam[l]), p_begin, p_stride, npiv)
             fresh = False
@@ -654,6 +655,44 @@ class DeviceFit:
         if piv.value < 0:
             return None
         return PivotWinner(int(piv.value), float(lam), vh, float(err.value), float(pen.value), float(obj.value))
+
+    def fit_lines_device(self, lams, p_begin: int, p_stride: int, npiv: int, ub_exchange=None,
+                         keep_ranges: bool = True) -> list[PivotWinner | None]:
+        """A pruned penalty sweep (>= 2 distinct finite penalties) via l1b_fit_lines: the cascade of
+        _sweep_winners in C++.  ``ub_exchange(tops) -> global tops`` (a vector over the distinct
+        penalties) is handed to the library as its exchange hook."""
+        lam = np.ascontiguousarray(np.asarray(lams, dtype=np.float64))
+        L = int(np.unique(lam).size)
+        failed = []
+
+        def _exchange(ptr, count, ctx):
+            try:
+                a = np.ctypeslib.as_array(ptr, shape=(count,))
+                a[:] = np.asarray(ub_exchange(a.copy()), dtype=np.float64).reshape(count)
+            except BaseException as e:  # noqa: BLE001 -- re-raised after the C call
+                failed.append(e)
+        hook = _lib.UB_EXCHANGE_VEC_FN(0) if ub_exchange is None else _lib.UB_EXCHANGE_VEC_FN(_exchange)
+        k = lam.size
+        piv = np.zeros(k, dtype=np.int64)
+        err, pen, obj = np.zeros(k), np.zeros(k), np.zeros(k)
+        cand = ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            bounds = torch.empty(2 * L * npiv, dtype=torch.float64, device=self.device)
+            rg = torch.empty(L * npiv * self.m * 2, dtype=torch.float32, device=self.device) if keep_ranges else None
+            V = torch.empty((k, self.m), dtype=torch.float64, device=self.device)
+            dp = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))  # noqa: E731
+            rc = self.lib.l1b_fit_lines(
+                self.X.data_ptr(), self.n, self.m, dp(lam, ctypes.c_double), k, p_begin, p_stride, npiv, hook, None,
+                bounds.data_ptr(), None if rg is None else rg.data_ptr(), 0 if rg is None else rg.numel() * 4,
+                dp(piv, ctypes.c_int64), V.data_ptr(), dp(err, ctypes.c_double), dp(pen, ctypes.c_double),
+                dp(obj, ctypes.c_double), ctypes.byref(cand), self.ws.data_ptr(), self.ws.numel(), self._s)
+            if failed:
+                raise failed[0]
+            _lib.check(rc, "l1b_fit_lines")
+            Vh = V.cpu().numpy()
+        self.last_candidates = int(cand.value)
+        return [None if piv[j] < 0 else PivotWinner(int(piv[j]), float(lam[j]), Vh[j].copy(), float(err[j]),
+                                                    float(pen[j]), float(obj[j])) for j in range(k)]
 
     def auto_prune(self) -> bool:
         """Whether shard_winners bounds before fitting: the bound pass costs a

@@ -415,6 +415,35 @@ def test_pruned_fit_equals_full_fit():
             assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
 
 
+def test_sweep_driver_matches_python_cascade(monkeypatch):
+    """l1b_fit_lines (the sweep cascade in C++) returns exactly what the same
+    cascade driven from Python returns (engine._sweep_winners): unsorted and
+    repeated penalties, and a global-threshold hook that leaves some penalties
+    to "another shard" (None)."""
+    d, _ = l1b.gen_line_data(300, 1500, seed=12, noise_scale=1.0)
+    X = d.values
+    T = float(np.abs(X).sum(axis=0).max())
+    lams = [5.0, 0.0, 1.0, 5.0, 0.3 * T, 0.05 * T]
+    eng = DeviceFit(X)
+
+    def run(py, exchange=None):
+        monkeypatch.setenv("L1B200_PY_SWEEP", "1" if py else "0")
+        return eng.shard_winners(lams, prune=True, ub_exchange=exchange)
+
+    for exchange in (None, lambda tops: np.where(np.arange(tops.size) % 2 == 0, tops * (1 - 1e-3), tops)):
+        a, b = run(False, exchange), run(True, exchange)
+        assert len(a) == len(b) == len(lams)
+        for x, y in zip(a, b):
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert x.pivot == y.pivot and x.v.tobytes() == y.v.tobytes()
+                assert (x.error, x.penalty_norm, x.objective, x.lam) == (y.error, y.penalty_norm, y.objective, y.lam)
+        if exchange is None:
+            full = eng.shard_winners(lams, prune=False)
+            assert [w.pivot for w in a] == [w.pivot for w in full]
+            assert all(w.v.tobytes() == f.v.tobytes() and w.objective == f.objective for w, f in zip(a, full))
+
+
 def test_raster_bands_leave_bounds_unchanged(monkeypatch):
     """k_bound's raster bands (CTAs pivot-group-major inside bands of target
     groups, used when the target tiles outgrow L2) only reorder the CTAs: the
