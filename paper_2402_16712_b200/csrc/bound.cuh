@@ -22,13 +22,14 @@
 // (v_p = 1).  A pivot whose lower bound exceeds the smallest upper bound
 // cannot win; the host fits only the others exactly (l1b_fit_pivot_list).
 //
-// Layout: a CTA is 4 pivots x 128 targets (512 problems) in 16 warps.  A
-// thread owns EIGHT problems, the four pivots x two targets (lane + 32 e) of
-// its warp's half of the tile; the 8 warps of a half split the rows.  Per
-// row a thread loads two x_ij and the four pivots' (y | x | w) records (three
-// broadcast 16-byte loads) and does 8 ratio elements, so the shared-memory
-// pipe carries 16 atomics + 4 tile + 12 record wavefronts per 512 elements
-// (k_bound below).
+// Layout: a CTA is 4 pivots x 64 targets (256 problems) in 8 warps, two CTAs
+// per SM (KB_TGT = 128: 16 warps, one CTA per SM -- slower, kept as a build
+// option).  A thread owns EIGHT problems, the four pivots x two targets
+// (lane, lane + 32); the 8 warps split each 64-row chunk's rows.  Per row a
+// thread loads its two x_ij (one 8-byte load) and the four pivots' (y | x | w)
+// records (three broadcast 16-byte loads) and does 8 ratio elements, so the
+// shared-memory pipe carries 8 atomics + 2 tile + 3 record wavefronts per 256
+// elements (k_bound below).
 
 #ifndef KB_TGT
 #define KB_TGT 64   // targets per CTA: 64 (8 warps, 2 CTAs per SM) or 128 (16 warps, 1 CTA per SM)
