@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kBpThreads) k_breakpoints(SelParams P, int64_t
   int* row = reinterpret_cast<int*>(psm + np2 * sizeof(unsigned long long));
   __shared__ int cnt_s;
   const int tid = threadIdx.x;
-  const int64_t n = P.n, m = P.m;
+  const int64_t n = P.n;
   const int64_t c = blockIdx.x;           // output column
   const int64_t cj = c0 + c;              // target column index among j != p
   const int64_t j = cj < p ? cj : cj + 1;

@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(kBS, 2) k_select(SelParams P) {
   const int64_t j = j0 + lane;
   const bool degenerate = piv_ok && P.nnz[p] == 0;
   const bool active = piv_ok && !degenerate && j < m && j != p;
-  const int64_t jc = j < m ? j : m - 1;
 
   double Tq = 0.0;
   double Lsc = 0.0;
