@@ -191,6 +191,13 @@ int l1b_absmax(const double* d_X, int64_t n, int64_t m, double* d_out, void* str
  * the copy engine reads it (hostcopy.inc). */
 int l1b_host_copy(void* dst, const void* src, size_t bytes, int32_t threads);
 
+/* Host -> device upload of `bytes` from pageable h_src through two pinned
+ * staging buffers of stage_bytes each (l1b_host_copy into one while the copy
+ * engine reads the other), all on `stream`; returns once the last transfer is
+ * queued (the staging buffers must not be reused before the stream passes it). */
+int l1b_upload(void* d_dst, const void* h_src, size_t bytes, void* h_stage0, void* h_stage1, size_t stage_bytes,
+               int32_t threads, void* stream);
+
 /* The same max_ij |x_ij| of the matrix the workspace was last prepared for
  * (l1b_prepare computes it with the column statistics): one 8-byte copy into
  * d_out[0] on the stream, no pass over X. */

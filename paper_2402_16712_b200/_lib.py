@@ -31,6 +31,7 @@ ABI_SYMBOLS = (
     "l1b_absmax",
     "l1b_prepared_absmax",
     "l1b_host_copy",
+    "l1b_upload",
     "l1b_selftest_divide",
     "l1b_kernel_launches",
     "l1b_dfma_probe",
@@ -127,6 +128,8 @@ def load() -> ctypes.CDLL:
     lib.l1b_absmax.argtypes = [_vp, _i64, _i64, _vp, _vp]
     lib.l1b_host_copy.restype = ctypes.c_int
     lib.l1b_host_copy.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int32]
+    lib.l1b_upload.restype = ctypes.c_int
+    lib.l1b_upload.argtypes = [_vp, _vp, ctypes.c_size_t, _vp, _vp, ctypes.c_size_t, ctypes.c_int32, _vp]
     lib.l1b_prepared_absmax.restype = ctypes.c_int
     lib.l1b_prepared_absmax.argtypes = [_vp, _i64, _i64, ctypes.c_size_t, _vp, _vp]
     lib.l1b_selftest_divide.restype = ctypes.c_int

@@ -77,31 +77,24 @@ _STAGE_THREADS = 8
 
 
 def _upload(Xh: np.ndarray, device: torch.device) -> torch.Tensor:
-    """Host numpy -> device through two reused pinned chunks: the CPU copy of
-    chunk i+1 into pinned memory overlaps the DMA of chunk i (instead of
-    pinning the whole matrix, then copying it).  The CPU copy is
+    """Host numpy -> device through two reused pinned chunks (l1b_upload): the
+    CPU copy of chunk i+1 into pinned memory overlaps the DMA of chunk i
+    (instead of pinning the whole matrix, then copying it).  The CPU copy is
     l1b_host_copy: a few pool threads with streaming stores, so the copy
     engine reads the chunk from DRAM at full link speed (hostcopy.inc)."""
     key = (device.type, device.index)
     if key not in _STAGING:
         with torch.cuda.device(device):
-            _STAGING[key] = [(torch.empty(_STAGE_DOUBLES, dtype=torch.float64).pin_memory(), torch.cuda.Event())
-                             for _ in range(2)]
+            _STAGING[key] = [torch.empty(_STAGE_DOUBLES, dtype=torch.float64).pin_memory() for _ in range(2)]
     stage = _STAGING[key]
     lib = _lib.load()
-    src = Xh.reshape(-1)
-    base = src.ctypes.data
     with torch.cuda.device(device):
         dst = torch.empty(Xh.shape, dtype=torch.float64, device=device)
-        flat = dst.view(-1)
         stream = torch.cuda.current_stream(device)
-        for i, off in enumerate(range(0, src.size, _STAGE_DOUBLES)):
-            k = min(_STAGE_DOUBLES, src.size - off)
-            buf, ev = stage[i & 1]
-            ev.synchronize()  # the DMA that last read this chunk has finished
-            _lib.check(lib.l1b_host_copy(buf.data_ptr(), base + 8 * off, 8 * k, _STAGE_THREADS), "l1b_host_copy")
-            flat[off:off + k].copy_(buf[:k], non_blocking=True)
-            ev.record(stream)
+        _lib.check(lib.l1b_upload(dst.data_ptr(), Xh.ctypes.data, Xh.nbytes, stage[0].data_ptr(), stage[1].data_ptr(),
+                                  8 * _STAGE_DOUBLES, _STAGE_THREADS, stream.cuda_stream), "l1b_upload")
+        # the stages are reused by the next upload: its first wait is on these transfers'
+        # events inside l1b_upload, so nothing else is needed here
     return dst
 
 

@@ -415,6 +415,25 @@ def test_pruned_fit_equals_full_fit():
             assert (a.error, a.penalty_norm, a.objective) == (b.error, b.penalty_norm, b.objective)
 
 
+def test_staged_upload_is_exact():
+    """engine._upload (l1b_upload: pooled streaming-store staging, two pinned
+    chunks, the first a quarter chunk): byte-identical device copies for sizes
+    around the chunk boundaries, several uploads queued back to back."""
+    from paper_2402_16712_b200 import engine
+    rng = np.random.default_rng(3)
+    ch = engine._STAGE_DOUBLES
+    dev = torch.device("cuda", torch.cuda.current_device())
+    outs = []
+    for rows, cols in [(1, 7), (ch // 4 // 8, 8), (ch // 4 // 8 + 1, 8), (ch // 1000, 1000), (3 * ch // 700 + 5, 700),
+                       (1234, 2345)]:
+        X = rng.standard_normal((rows, cols))
+        X[0, 0] = -0.0
+        outs.append((X, engine._upload(X, dev)))  # no synchronisation between uploads
+    torch.cuda.synchronize()
+    for X, d in outs:
+        assert d.cpu().numpy().tobytes() == X.tobytes(), X.shape
+
+
 def test_sweep_driver_matches_python_cascade(monkeypatch):
     """l1b_fit_lines (the sweep cascade in C++) returns exactly what the same
     cascade driven from Python returns (engine._sweep_winners): unsorted and
