@@ -166,6 +166,19 @@ def test_abi_workspace_and_argument_checks():
     assert lib.l1b_fit_pivots(1, 5, 4, lam, 1, 0, 1, 4, None, 1, 1, 1, 1, 1 << 30, None) == _lib.L1B_EINVAL
     lam[0] = 1.0
     assert lib.l1b_fit_pivots(1, 5, 4, lam, 1, 3, 1, 2, None, 1, 1, 1, 1, 1 << 30, None) == _lib.L1B_EINVAL
+    # l1b_fit_lines: >= 2 distinct finite nonnegative penalties, a valid shard
+    hook = _lib.UB_EXCHANGE_VEC_FN(0)
+    out_i = (ctypes.c_int64 * 3)()
+    out_d = [(ctypes.c_double * 3)() for _ in range(3)]
+
+    def fit_lines(vals, p_begin=0, npiv=4):
+        lams = (ctypes.c_double * len(vals))(*vals)
+        return lib.l1b_fit_lines(1, 5, 4, lams, len(vals), p_begin, 1, npiv, hook, None, 1, None, 0, out_i, 1,
+                                 out_d[0], out_d[1], out_d[2], None, 1, 1 << 30, None)
+    assert fit_lines([1.0, 1.0]) == _lib.L1B_EINVAL             # one distinct penalty: l1b_fit_line
+    assert fit_lines([1.0, float("inf")]) == _lib.L1B_EINVAL    # non-finite
+    assert fit_lines([1.0, -2.0]) == _lib.L1B_EINVAL            # negative
+    assert fit_lines([1.0, 2.0], p_begin=3, npiv=2) == _lib.L1B_EINVAL  # shard past the last pivot
 
 
 def test_abi_sass_is_sm100a():
