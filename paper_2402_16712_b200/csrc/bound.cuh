@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
       ec[t][ee] = 0.0;
     }
   int nflush = 0;
+  const bool e1_dead = (tile0 + th * kBTE + 1) * 32 >= m;  // targets of slot e = 1 all past column m - 1
   for (int64_t c = 0; c < nch; ++c) {
     const int st = (int)(c % kBStages);
     mbar_wait(&full[st], (fphase >> st) & 1u);
@@ -658,47 +659,54 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) k_bound(SelParams P) {
     const unsigned char* sb = smem + (size_t)st * kBStage;
     const float2* ta = (const float2*)sb + th * 32 + lane;  // [kBRows][half][lane]: this thread's two targets
     const float4* rec = (const float4*)(sb + kBTile);       // [kBRows][3]
+    // the thread's second target slot past the last column (the ragged last
+    // group): a warp-uniform half-width body
+    auto rows = [&](auto ne) {
+      constexpr int NE = decltype(ne)::value;
 #pragma unroll
-    for (int u2 = 0; u2 < kBRowsW; u2 += 2) {
-      float2 rr[2][kBPiv / 2][kBTE];  // x_ij - c x_ip of the row pair, pivots (2h, 2h + 1)
+      for (int u2 = 0; u2 < kBRowsW; u2 += 2) {
+        float2 rr[2][kBPiv / 2][kBTE];  // x_ij - c x_ip of the row pair, pivots (2h, 2h + 1)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int r = rg * kBRowsW + u2 + v;
-        static_assert(kBTE == 2, "one 8-byte load per row");
-        const float2 xv = ta[r * (kBTgt / 2)];
-        const float x[kBTE] = {xv.x, xv.y};
-        const float4 Y = rec[r * 3], X = rec[r * 3 + 1], W = rec[r * 3 + 2];
+        for (int v = 0; v < 2; ++v) {
+          const int r = rg * kBRowsW + u2 + v;
+          static_assert(kBTE == 2, "one 8-byte load per row");
+          const float2 xv = ta[r * (kBTgt / 2)];
+          const float x[kBTE] = {xv.x, xv.y};
+          const float4 Y = rec[r * 3], X = rec[r * 3 + 1], W = rec[r * 3 + 2];
 #pragma unroll
-        for (int h = 0; h < kBPiv / 2; ++h) {
-          const float2 yy = h ? make_float2(Y.z, Y.w) : make_float2(Y.x, Y.y);
-          const float2 xx = h ? make_float2(X.z, X.w) : make_float2(X.x, X.y);
-          const unsigned w0 = __float_as_uint(h ? W.z : W.x), w1 = __float_as_uint(h ? W.w : W.y);
+          for (int h = 0; h < kBPiv / 2; ++h) {
+            const float2 yy = h ? make_float2(Y.z, Y.w) : make_float2(Y.x, Y.y);
+            const float2 xx = h ? make_float2(X.z, X.w) : make_float2(X.x, X.y);
+            const unsigned w0 = __float_as_uint(h ? W.z : W.x), w1 = __float_as_uint(h ? W.w : W.y);
 #pragma unroll
-          for (int ee = 0; ee < kBTE; ++ee) {
-            const float2 q = fmul2(make_float2(x[ee], x[ee]), yy);
-            const float2 bb = ffma2(make_float2(__saturatef(fmaf(q.x, A[2 * h][ee], B[2 * h][ee])),
-                                                __saturatef(fmaf(q.y, A[2 * h + 1][ee], B[2 * h + 1][ee]))),
-                                    make_float2(63.f, 63.f), make_float2(8388608.f, 8388608.f));
-            const unsigned a0 = hb + __float_as_uint(bb.x) * (unsigned)(kBTgt * 4) +
-                                (unsigned)(((2 * h) * kNB * kBTgt + ee * 32) * 4);
-            const unsigned a1 = hb + __float_as_uint(bb.y) * (unsigned)(kBTgt * 4) +
-                                (unsigned)(((2 * h + 1) * kNB * kBTgt + ee * 32) * 4);
-            // fire-and-forget shared adds (the other warps add into the same bins)
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(w0));
-            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1), "r"(w1));
-            // x_ij - c x_ip of both pivots (dropped rows: x_ij)
-            rr[v][h][ee] = ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee]));
+            for (int ee = 0; ee < NE; ++ee) {
+              const float2 q = fmul2(make_float2(x[ee], x[ee]), yy);
+              const float2 bb = ffma2(make_float2(__saturatef(fmaf(q.x, A[2 * h][ee], B[2 * h][ee])),
+                                                  __saturatef(fmaf(q.y, A[2 * h + 1][ee], B[2 * h + 1][ee]))),
+                                      make_float2(63.f, 63.f), make_float2(8388608.f, 8388608.f));
+              const unsigned a0 = hb + __float_as_uint(bb.x) * (unsigned)(kBTgt * 4) +
+                                  (unsigned)(((2 * h) * kNB * kBTgt + ee * 32) * 4);
+              const unsigned a1 = hb + __float_as_uint(bb.y) * (unsigned)(kBTgt * 4) +
+                                  (unsigned)(((2 * h + 1) * kNB * kBTgt + ee * 32) * 4);
+              // fire-and-forget shared adds (the other warps add into the same bins)
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(w0));
+              asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a1), "r"(w1));
+              // x_ij - c x_ip of both pivots (dropped rows: x_ij)
+              rr[v][h][ee] = ffma2(nc[h][ee], xx, make_float2(x[ee], x[ee]));
+            }
           }
         }
+        // the row pair's |terms| summed first, then added (two FADD2 per four
+        // elements; the pair sums keep the accumulation error at 16 u per flush)
+#pragma unroll
+        for (int h = 0; h < kBPiv / 2; ++h)
+#pragma unroll
+          for (int ee = 0; ee < NE; ++ee)
+            racc[h][ee] = fadd2(racc[h][ee], fadd2(fabs2(rr[0][h][ee]), fabs2(rr[1][h][ee])));
       }
-      // the row pair's |terms| summed first, then added (two FADD2 per four
-      // elements; the pair sums keep the accumulation error at 16 u per flush)
-#pragma unroll
-      for (int h = 0; h < kBPiv / 2; ++h)
-#pragma unroll
-        for (int ee = 0; ee < kBTE; ++ee)
-          racc[h][ee] = fadd2(racc[h][ee], fadd2(fabs2(rr[0][h][ee]), fabs2(rr[1][h][ee])));
-    }
+    };
+    if (e1_dead) rows(std::integral_constant<int, 1>{});
+    else rows(std::integral_constant<int, kBTE>{});
     if (++nflush == KB_FLUSH || c + 1 == nch) {
       nflush = 0;
 #pragma unroll
